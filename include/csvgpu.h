@@ -1,0 +1,147 @@
+/*
+ * csvgpu.h -- C-ABI of the B200-native CSV brick decoder (libcsvgpu.so).
+ *
+ * The reference (`csvol`, pure Python + numba) has no FFI; its decode entry
+ * points are in-process numba calls.  Each function below replaces one of
+ * them (citations: /root/reference/pkg/src/csvol/<file>:<line>), exported
+ * with plain pointers and sizes so any host language can bind it (the Python
+ * host in paper_2308_16619_b200/ binds it with ctypes).
+ *
+ * Conventions:
+ *   - Every function returns CSV_OK (0) or a negative CSV_E_* code; the text
+ *     of the last failure on the calling thread is csv_last_error().
+ *   - Device pointers ("d_" prefix) are caller-owned device memory; the
+ *     library never frees caller memory.  Compressed data uploaded by
+ *     csv_volume_create is library-owned until csv_volume_free.
+ *   - All decode calls are asynchronous on the caller's CUDA stream
+ *     (`stream` is a cudaStream_t cast to uintptr_t; 0 = legacy default).
+ *     A csv_volume owns one workspace: calls on one volume must be ordered
+ *     on one stream (use one volume handle per concurrent stream).
+ *   - Per-brick corruption is NOT a call failure: it is reported per brick
+ *     in csv_result with the reference's status codes (codec.py:280-287),
+ *     stream and nibble position, so the host raises byte-identical
+ *     CorruptStreamError messages (codec.py:487-495, :540-543).
+ */
+#ifndef CSVGPU_H
+#define CSVGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSV_OK 0
+#define CSV_E_ARG (-1)      /* invalid argument */
+#define CSV_E_CUDA (-2)     /* CUDA runtime error */
+#define CSV_E_NOMEM (-3)    /* device allocation failed */
+#define CSV_E_FORMAT (-4)   /* malformed container header */
+
+/* Per-brick status codes: 0..7 as codec.py:280-287, plus CSV_ST_EMPTY_PALETTE
+ * for codec.py:510-511 ("empty palette"). */
+#define CSV_ST_OK 0
+#define CSV_ST_UNDERRUN 1
+#define CSV_ST_BAD_OP 2
+#define CSV_ST_PALETTE_RANGE 3
+#define CSV_ST_DELTA_RANGE 4
+#define CSV_ST_DESYNC 5
+#define CSV_ST_BAD_NEIGHBOR 6
+#define CSV_ST_LEAF_STOP 7
+#define CSV_ST_EMPTY_PALETTE 8
+
+/* One decode outcome; mirrors the tuple _decode_kernel returns
+ * (codec.py:322: status, stream, nibble position, consumed coarse, consumed detail). */
+typedef struct csv_result {
+    int32_t status;
+    int32_t stream;   /* 0 coarse, 1 detail */
+    int64_t pos;      /* nibble position of the failure */
+    int64_t ci;       /* coarse nibbles consumed (valid when status == 0) */
+    int64_t di;       /* detail nibbles consumed (valid when status == 0) */
+} csv_result;
+
+/* K1 per-stream outcome (csv_decode_streams). */
+typedef struct csv_stream_result {
+    uint32_t n_entries;    /* complete entries (op nibble + payload) decoded */
+    uint32_t fail_nibble;  /* first unavailable nibble (flags & CSV_SF_FAILED) */
+    uint32_t flags;        /* CSV_SF_* */
+    uint32_t partial_op;   /* op nibble of entry n_entries when CSV_SF_PARTIAL */
+} csv_stream_result;
+#define CSV_SF_FAILED 1u    /* nibble fail_nibble cannot be pulled (underrun / count exhausted) */
+#define CSV_SF_PARTIAL 2u   /* entry n_entries has its op nibble but no payload */
+#define CSV_SF_DESYNC 4u    /* all nibbles decoded; final state != 2^23 or bytes left (rans.py:163) */
+#define CSV_SF_COMPLETE 8u  /* all `n` nibbles decoded */
+
+typedef struct csv_volume csv_volume;
+
+/* Library/version probe. */
+int csv_version(void);
+const char* csv_last_error(void);
+
+/* Volume upload from HOST memory.  Replaces CsvContainer._parse_head /
+ * _parse_body (container.py:289-330) as the decoder's input stage.
+ *   head120   : bytes 0..119 of the CSV1 file (header, both count tables, blob sizes)
+ *   dir44     : directory rows [brick_begin, brick_end), 44 B each (container.py:53-64)
+ *   palette   : u32 palette entries starting at global entry palette_base
+ *   coarse    : coarse-blob bytes starting at global byte coarse_base
+ *   detail    : detail-blob bytes starting at global byte detail_base (may be NULL/0)
+ * Directory offsets are global; rows pointing outside the passed slices are
+ * clamped like numpy slicing (container.py:138-153).  Copies are issued on
+ * `stream`; host buffers may be reused once the stream has passed this call. */
+int csv_volume_create(int device, const uint8_t* head120, const uint8_t* dir44,
+                      uint64_t brick_begin, uint64_t brick_end,
+                      const uint32_t* palette, uint64_t palette_base, uint64_t palette_len,
+                      const uint8_t* coarse, uint64_t coarse_base, uint64_t coarse_len,
+                      const uint8_t* detail, uint64_t detail_base, uint64_t detail_len,
+                      uintptr_t stream, csv_volume** vol);
+
+/* Same, from DEVICE memory already resident (e.g. the GPU encoder's output).
+ * The blobs are borrowed (not copied): keep them alive until csv_volume_free. */
+int csv_volume_create_device(int device, const uint8_t* head120, const uint8_t* d_dir44,
+                             uint64_t brick_begin, uint64_t brick_end,
+                             const uint32_t* d_palette, uint64_t palette_base, uint64_t palette_len,
+                             const uint8_t* d_coarse, uint64_t coarse_base, uint64_t coarse_len,
+                             const uint8_t* d_detail, uint64_t detail_base, uint64_t detail_len,
+                             uintptr_t stream, csv_volume** vol);
+
+int csv_volume_free(csv_volume* vol);
+
+/* Full-volume decode at LOD t into a raster (Z,Y,X) u32 slab: replaces
+ * decompress_volume (container.py:456-478) + morton_to_grid (morton.py:411-416).
+ * d_out holds LOD-t z rows [z_begin, z_end) of the volume cropped to
+ * ceil(dims / 2^t) (container.py:476-478); only this volume's bricks are
+ * decoded.  d_res (may be NULL) receives one csv_result per brick of the
+ * volume's range, in brick order. */
+int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, int64_t z_end,
+                      csv_result* d_res, uintptr_t stream);
+
+/* Batched random-access decode into a Morton-order brick pool: replaces the
+ * per-brick CsvContainer.decode_brick (container.py:168-208) loop inside
+ * BrickCache._store / end_frame_assign (cache.py:125-170).  Request i decodes
+ * brick d_brick[i] (global index) at LOD d_lod[i] into
+ * d_pool[d_dst[i] .. d_dst[i] + 8^(N - lod)) in Morton order (cache.py:130-134).
+ * Requests must target disjoint pool ranges.  d_res receives one csv_result
+ * per request (may be NULL). */
+int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, const uint8_t* d_lod,
+                      const uint64_t* d_dst, uint32_t* d_pool, csv_result* d_res, uintptr_t stream);
+
+/* Stand-alone entropy stage (K1): replaces rans_decode/_decode_core
+ * (rans.py:140-198) + iter_operations (codec.py:604-623).  For each request
+ * brick, decodes the coarse and (t == 0) detail stream into entry bytes
+ * (op | stop<<3 | delta<<4, one per operation) at d_entries + d_entry_off[2i+s],
+ * s = 0 coarse / 1 detail.  d_entry_off must hold 2n+1 u64 and is filled with
+ * the exclusive scan of the per-stream regions; d_sres receives 2n results.
+ * entries_cap is the capacity of d_entries in bytes. */
+int csv_decode_streams(csv_volume* vol, uint64_t n, const uint32_t* d_brick, int t,
+                       uint8_t* d_entries, uint64_t entries_cap, uint64_t* d_entry_off,
+                       csv_stream_result* d_sres, uintptr_t stream);
+
+/* Upper bound of the entry bytes csv_decode_streams needs for n requests at LOD t. */
+int csv_streams_capacity(csv_volume* vol, uint64_t n, int t, uint64_t* cap);
+
+/* Volume geometry probe: dims(x,y,z), grid(x,y,z), brick_log2, entropy. */
+int csv_volume_info(csv_volume* vol, int64_t* dims3, int64_t* grid3, int* brick_log2, int* entropy);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSVGPU_H */

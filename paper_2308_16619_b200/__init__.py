@@ -1,0 +1,27 @@
+"""B200-native decoder for CSV compressed segmentation volumes (arXiv 2308.16619).
+
+Drop-in for the reference ``csvol`` decode/brick-access API: same names,
+argument meaning and errors; the per-brick decompression (rANS entropy
+decode + coarse-to-fine operation replay) runs in hand-written sm_100a CUDA
+kernels (csrc/) reached through the C-ABI in include/csvgpu.h.
+"""
+
+from .cache import BrickCache, CacheStats
+from .codec import BrickEncoding, decode_brick, decode_brick_entropy, decode_root, iter_operations
+from .container import (CompressionConfig, CsvContainer, VolumeMeta, decompress_volume,
+                        decompress_volume_device)
+from .device import GpuVolume
+from .errors import (CacheCapacityError, ConfigError, CorruptStreamError, CsvolError, EncodabilityError,
+                     IngestionError)
+from .morton import BrickConfig, NodeCoord, morton_decode, morton_encode, outside_neighbor
+from .rans import FrequencyTable, TablePair, build_frequency_tables, quantize_counts
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BrickCache", "BrickConfig", "BrickEncoding", "CacheCapacityError", "CacheStats", "CompressionConfig",
+    "ConfigError", "CorruptStreamError", "CsvContainer", "CsvolError", "EncodabilityError", "FrequencyTable",
+    "GpuVolume", "IngestionError", "NodeCoord", "TablePair", "VolumeMeta", "build_frequency_tables",
+    "decode_brick", "decode_brick_entropy", "decode_root", "decompress_volume", "decompress_volume_device",
+    "iter_operations", "morton_decode", "morton_encode", "outside_neighbor", "quantize_counts",
+]

@@ -1,0 +1,79 @@
+"""ctypes binding of libcsvgpu.so (C-ABI declared in include/csvgpu.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is visible, every decode entry point raises ``RuntimeError`` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libcsvgpu.so")
+_lib = None
+
+RESULT_DTYPE = np.dtype([("status", "<i4"), ("stream", "<i4"), ("pos", "<i8"), ("ci", "<i8"), ("di", "<i8")])
+STREAM_RESULT_DTYPE = np.dtype([("n_entries", "<u4"), ("fail_nibble", "<u4"), ("flags", "<u4"), ("partial_op", "<u4")])
+
+EXPORTS = (
+    "csv_version", "csv_last_error", "csv_volume_create", "csv_volume_create_device", "csv_volume_free",
+    "csv_decode_volume", "csv_decode_bricks", "csv_decode_streams", "csv_streams_capacity", "csv_volume_info",
+)
+
+
+def build(force: bool = False) -> str:
+    """Compile the CUDA sources for sm_100a into the package directory."""
+    csrc = os.path.join(_PKG, "csrc")
+    srcs = [os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith((".cu", ".cuh"))]
+    srcs.append(os.path.join(os.path.dirname(_PKG), "include", "csvgpu.h"))
+    newest = max(os.path.getmtime(s) for s in srcs)
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
+        subprocess.run(["make", "-s", "-C", csrc], check=True)
+    return LIB_PATH
+
+
+def lib():
+    """Load libcsvgpu.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, U64, I64, I, UP = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+        L.csv_version.restype = I
+        L.csv_last_error.restype = ctypes.c_char_p
+        L.csv_volume_create.restype = I
+        L.csv_volume_create.argtypes = [I, P, P, U64, U64, P, U64, U64, P, U64, U64, P, U64, U64, UP, P]
+        L.csv_volume_create_device.restype = I
+        L.csv_volume_create_device.argtypes = [I, P, P, U64, U64, P, U64, U64, P, U64, U64, P, U64, U64, UP, P]
+        L.csv_volume_free.restype = I
+        L.csv_volume_free.argtypes = [P]
+        L.csv_decode_volume.restype = I
+        L.csv_decode_volume.argtypes = [P, I, P, I64, I64, P, UP]
+        L.csv_decode_bricks.restype = I
+        L.csv_decode_bricks.argtypes = [P, U64, P, P, P, P, P, UP]
+        L.csv_decode_streams.restype = I
+        L.csv_decode_streams.argtypes = [P, U64, P, I, P, U64, P, P, UP]
+        L.csv_streams_capacity.restype = I
+        L.csv_streams_capacity.argtypes = [P, U64, I, P]
+        L.csv_volume_info.restype = I
+        L.csv_volume_info.argtypes = [P, P, P, P, P]
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().csv_last_error().decode(errors="replace")
+        raise RuntimeError(f"libcsvgpu error {rc}: {msg}")
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2308_16619_b200 decodes on a CUDA device; none is visible (no CPU fallback)")
+    return torch

@@ -1,0 +1,178 @@
+"""Brick codec API: palette + coarse/detail operation streams (csvol/codec.py).
+
+Opcode table (codec.py:9-20, :49-65): each child entry is a nibble
+``(stop << 3) | op``; op 5 (palette back-reference) is followed by a payload
+nibble delta.  Decoding here runs on the GPU: every function below builds a
+one-brick device volume and calls the batched K1/K2 kernels through the
+C-ABI, returning Morton-ordered labels exactly as the reference does.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import CorruptStreamError
+from .morton import BrickConfig
+from .rans import FrequencyTable, TablePair
+
+OP_PARENT = 0
+OP_NEIGHBOR_X = 1
+OP_NEIGHBOR_Y = 2
+OP_NEIGHBOR_Z = 3
+OP_PALETTE_LAST = 4
+OP_PALETTE_DELTA = 5
+OP_PALETTE_ADVANCE = 6
+
+OP_NAMES = {
+    OP_PARENT: "parent",
+    OP_NEIGHBOR_X: "neighbor_x",
+    OP_NEIGHBOR_Y: "neighbor_y",
+    OP_NEIGHBOR_Z: "neighbor_z",
+    OP_PALETTE_LAST: "palette_last",
+    OP_PALETTE_DELTA: "palette_back",
+    OP_PALETTE_ADVANCE: "palette_advance",
+}
+
+_HEADER = struct.Struct("<4sHBBHH3III")
+_BLOBS = struct.Struct("<3Q")
+DIRECTORY_DTYPE = np.dtype([
+    ("palette_off", "<u8"), ("palette_len", "<u4"),
+    ("coarse_off", "<u8"), ("coarse_bytes", "<u4"), ("coarse_nibbles", "<u4"),
+    ("detail_off", "<u8"), ("detail_bytes", "<u4"), ("detail_nibbles", "<u4"),
+])
+
+
+@dataclass(frozen=True)
+class BrickEncoding:
+    """Palette and raw (pre-entropy) nibble streams of one brick (codec.py:70-90)."""
+
+    brick_log2: int
+    palette: np.ndarray
+    coarse: np.ndarray
+    detail: np.ndarray
+
+    @property
+    def config(self) -> BrickConfig:
+        return BrickConfig(self.brick_log2)
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, BrickEncoding) and self.brick_log2 == other.brick_log2
+                and np.array_equal(self.palette, other.palette) and np.array_equal(self.coarse, other.coarse)
+                and np.array_equal(self.detail, other.detail))
+
+
+def pack_nibbles(nibbles: np.ndarray) -> np.ndarray:
+    """Two nibbles per byte, low nibble first (container.py:340-345)."""
+    nib = np.asarray(nibbles, dtype=np.uint8)
+    if nib.size % 2:
+        nib = np.concatenate([nib, np.zeros(1, np.uint8)])
+    return (nib[0::2] | (nib[1::2] << 4)).astype(np.uint8)
+
+
+def unpack_nibbles(packed: np.ndarray, count: int) -> np.ndarray:
+    out = np.empty(2 * packed.size, dtype=np.uint8)
+    out[0::2] = packed & 0x0F
+    out[1::2] = packed >> 4
+    return out[:count]
+
+
+def single_brick_head(brick_log2: int, entropy: bool, tables: TablePair | None,
+                      n_pal: int, n_coarse: int, n_detail: int) -> bytes:
+    """120-byte CSV1 head of a one-brick volume (layout: container.py:3-18)."""
+    b = 1 << brick_log2
+    head = _HEADER.pack(b"CSV1", 1, 1 if entropy else 0, 0, 32, brick_log2, b, b, b, 512, 0)
+    t = tables or TablePair(FrequencyTable.uniform(), FrequencyTable.uniform())
+    head += t.interior.counts.astype("<u2").tobytes() + t.leaf.counts.astype("<u2").tobytes()
+    head += _BLOBS.pack(4 * n_pal, n_coarse, n_detail)
+    return head
+
+
+def _decode_one(palette, coarse, n_coarse, detail, n_detail, entropy, tables, config: BrickConfig, t,
+                return_consumed):
+    """_run_decode (codec.py:498-546) on the GPU for one brick."""
+    from .device import GpuVolume, status_error
+    from . import _lib
+    palette = np.asarray(palette)
+    if palette.size == 0:
+        raise CorruptStreamError("empty palette")
+    N = config.brick_log2
+    if not 0 <= t <= N:
+        raise ValueError(f"target LOD {t} outside [0, {N}]")
+    if t == N:
+        out = palette[:1].astype(np.uint32)
+        return (out, 0, 0) if return_consumed else out
+    torch = _lib.require_cuda()
+    pal = np.ascontiguousarray(palette, dtype=np.uint32)
+    cb = np.ascontiguousarray(coarse, dtype=np.uint8)
+    db = np.ascontiguousarray(detail, dtype=np.uint8)
+    row = np.zeros(1, dtype=DIRECTORY_DTYPE)
+    row["palette_len"] = pal.size
+    row["coarse_bytes"] = cb.size
+    row["coarse_nibbles"] = n_coarse
+    row["detail_bytes"] = db.size
+    row["detail_nibbles"] = n_detail
+    head = single_brick_head(N, entropy, tables, pal.size, cb.size, db.size)
+    vol = GpuVolume(head, row, pal, cb, db)
+    try:
+        dev = vol.device
+        bricks = torch.zeros(1, dtype=torch.int32, device=dev)
+        lods = torch.full((1,), t, dtype=torch.uint8, device=dev)
+        dst = torch.zeros(1, dtype=torch.int64, device=dev)
+        pool = torch.empty(8 ** (N - t), dtype=torch.int32, device=dev)
+        res = vol.decode_bricks(bricks, lods, dst, pool)
+        r = GpuVolume.results_host(res, 1)[0]
+        if r["status"] != 0:
+            raise status_error(int(r["status"]), int(r["stream"]), int(r["pos"]))
+        out = pool.cpu().numpy().view(np.uint32)
+    finally:
+        vol.close()
+    if return_consumed:
+        return out, int(r["ci"]), int(r["di"])
+    return out
+
+
+def decode_brick(encoding: BrickEncoding, t: int, config: BrickConfig | None = None, return_consumed: bool = False):
+    """Raw (pre-entropy) streams -> Morton-ordered level-t labels (codec.py:549-568).
+
+    The nibble arrays are packed two per byte for the device; streams hold
+    4-bit symbols (the payload of op 5 is one nibble, SPEC delta in [0, 15]).
+    """
+    config = config or encoding.config
+    c = np.asarray(encoding.coarse, dtype=np.uint8)
+    d = np.asarray(encoding.detail, dtype=np.uint8)
+    if (c.size and c.max() > 15) or (d.size and d.max() > 15):
+        raise ValueError("raw nibble streams must hold 4-bit symbols")
+    return _decode_one(encoding.palette, pack_nibbles(c), c.size, pack_nibbles(d), d.size, False, None,
+                       config, t, return_consumed)
+
+
+def decode_brick_entropy(palette, coarse_bytes, coarse_nibbles: int, detail_bytes, detail_nibbles: int,
+                         tables: TablePair, t: int, config: BrickConfig, return_consumed: bool = False):
+    """Entropy-coded streams -> Morton-ordered level-t labels (codec.py:571-594)."""
+    return _decode_one(palette, coarse_bytes, coarse_nibbles, detail_bytes, detail_nibbles, True, tables,
+                       config, t, return_consumed)
+
+
+def decode_root(encoding: BrickEncoding) -> int:
+    """Coarsest-LOD label (codec.py:597-601)."""
+    if encoding.palette.size == 0:
+        raise CorruptStreamError("empty palette")
+    return int(encoding.palette[0])
+
+
+def iter_operations(nibbles: np.ndarray):
+    """(opcode, stop, delta) triples of one raw nibble stream (codec.py:604-623)."""
+    i, n = 0, nibbles.size
+    while i < n:
+        nib = int(nibbles[i])
+        i += 1
+        op, stop, delta = nib & 7, nib >> 3, None
+        if op == OP_PALETTE_DELTA:
+            if i >= n:
+                raise CorruptStreamError(f"stream underrun (payload nibble {i})")
+            delta = int(nibbles[i])
+            i += 1
+        yield op, stop, delta

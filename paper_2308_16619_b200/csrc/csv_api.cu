@@ -1,0 +1,410 @@
+// csv_api.cu -- C-ABI of libcsvgpu.so (declared in include/csvgpu.h).
+//
+// Owns the per-volume device state: directory unpacked to SoA, the three
+// blobs (+16 B tail padding), packed decode tables, and a grow-only decode
+// workspace.  All entry points are extern "C" with plain pointers; see the
+// header for the reference function each one replaces.
+#include <cstdio>
+#include <cstring>
+#include <cstdarg>
+#include <string>
+#include <vector>
+#include <algorithm>
+#include "csv_device.cuh"
+
+namespace csv {
+cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, uint64_t* scan_tmp,
+                       unsigned long long* counter, uint32_t* gws, uint64_t gws_stride, int gws_ctas,
+                       int nsm, int min_t, cudaStream_t st);
+cudaError_t run_root_raster(const VolView& V, Plan P, cudaStream_t st);
+cudaError_t run_streams_only(const VolView& V, Plan P, uint64_t* sizes_tmp, uint64_t* scan_tmp,
+                             unsigned long long* counter, int nsm, cudaStream_t st);
+size_t k2_smem_bytes(int L);
+}  // namespace csv
+
+using namespace csv;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+#define CUDA_TRY(x)                                                                         \
+    do {                                                                                    \
+        cudaError_t e_ = (x);                                                               \
+        if (e_ != cudaSuccess) return fail(CSV_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+    } while (0)
+
+struct csv_volume {
+    int device = 0;
+    VolView V{};
+    void* d_soa = nullptr;          // directory SoA columns
+    uint8_t* d_blob = nullptr;      // owned blobs (host upload) or nullptr (borrowed)
+    uint32_t* d_dtab = nullptr;
+    // workspace (grow-only)
+    uint64_t plan_cap = 0;          // requests
+    uint64_t* d_sizes = nullptr;    // 2*cap
+    uint64_t* d_eoff = nullptr;     // 2*cap + 1
+    uint64_t* d_scan = nullptr;     // 4097
+    csv_stream_result* d_sres = nullptr;
+    unsigned long long* d_counter = nullptr;
+    uint8_t* d_entries = nullptr;
+    uint64_t entries_cap = 0;
+    uint32_t* d_gws = nullptr;
+    uint64_t gws_stride = 0;
+    int gws_ctas = 0;
+    uint64_t gws_words_cap = 0;
+    int nsm = 148;
+    uint64_t region_total_t0 = 0;   // sum over bricks of entry regions at t=0 (bytes)
+    uint64_t region_max_t0 = 0;     // max over bricks
+    int64_t dims[3]{}, grid[3]{};
+};
+
+// ---------------------------------------------------------------------------- kernels local to the API
+// Unpack 44-byte directory rows (container.py:53-64) into SoA, rebasing global
+// blob offsets to the uploaded slices and clamping lengths like numpy slicing.
+__global__ void k_unpack_dir(const uint8_t* dir44, uint64_t n, uint64_t pal_base, uint64_t pal_len,
+                             uint64_t c_base, uint64_t c_len, uint64_t d_base, uint64_t d_len,
+                             uint64_t* pal_off, uint32_t* pal_n, uint64_t* c_off, uint32_t* c_bytes,
+                             uint32_t* c_nib, uint64_t* d_off, uint32_t* d_bytes, uint32_t* d_nib) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t* p = dir44 + 44 * i;
+    auto u64 = [&](int o) { uint64_t v = 0; for (int k = 7; k >= 0; --k) v = (v << 8) | p[o + k]; return v; };
+    auto u32 = [&](int o) { uint32_t v = 0; for (int k = 3; k >= 0; --k) v = (v << 8) | p[o + k]; return v; };
+    auto clamp = [](uint64_t off, uint64_t len, uint64_t base, uint64_t avail, uint64_t* ooff) -> uint64_t {
+        // slice blob[off : off+len] of the global blob, of which [base, base+avail) was uploaded
+        if (off < base || off >= base + avail) { *ooff = 0; return 0; }
+        uint64_t rel = off - base;
+        uint64_t l = avail - rel;
+        *ooff = rel;
+        return len < l ? len : l;
+    };
+    uint64_t o;
+    pal_n[i] = (uint32_t)clamp(u64(0), u32(8), pal_base, pal_len, &o);
+    pal_off[i] = o;
+    c_bytes[i] = (uint32_t)clamp(u64(12), u32(20), c_base, c_len, &o);
+    c_off[i] = o;
+    c_nib[i] = u32(24);
+    d_bytes[i] = (uint32_t)clamp(u64(28), u32(36), d_base, d_len, &o);
+    d_off[i] = o;
+    d_nib[i] = u32(40);
+}
+
+__global__ void k_region_stats(VolView V, unsigned long long* total, unsigned long long* mx) {
+    uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    unsigned long long s = 0;
+    if (b < V.nb && V.N > 0) s = round16(stream_limit(V, b, 0, 0)) + round16(stream_limit(V, b, 0, 1));
+    unsigned long long m = s;
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        unsigned long long u = __shfl_xor_sync(0xffffffffu, m, o);
+        m = m > u ? m : u;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(total, s);
+        atomicMax(mx, m);
+    }
+}
+
+// ---------------------------------------------------------------------------- helpers
+static int parse_head(const uint8_t* h, csv_volume* v, uint32_t* dtab_host) {
+    if (memcmp(h, "CSV1", 4) != 0) return fail(CSV_E_FORMAT, "bad magic");
+    uint16_t version; memcpy(&version, h + 4, 2);
+    if (version != 1) return fail(CSV_E_FORMAT, "unsupported container version %u", version);
+    uint8_t flags = h[6];
+    uint16_t bl2; memcpy(&bl2, h + 10, 2);
+    uint32_t d3[3]; memcpy(d3, h + 12, 12);
+    if (bl2 < 1 || bl2 > 7) return fail(CSV_E_FORMAT, "brick_log2 must be in [1, 7], got %u", bl2);
+    v->V.N = bl2;
+    v->V.entropy = flags & 1;
+    int64_t b = 1ll << bl2;
+    for (int k = 0; k < 3; ++k) {
+        v->dims[k] = d3[k];
+        v->grid[k] = (d3[k] + b - 1) / b;
+    }
+    v->V.X = d3[0]; v->V.Y = d3[1]; v->V.Z = d3[2];
+    v->V.gx = v->grid[0]; v->V.gy = v->grid[1]; v->V.gz = v->grid[2];
+    // packed decode tables {freq:16 | (slot-cum):12 | sym:4} (rans.py:31-62, codec.py:290-300)
+    for (int tb = 0; tb < 2; ++tb) {
+        uint16_t cnt[16];
+        memcpy(cnt, h + 32 + 32 * tb, 32);
+        uint32_t sum = 0;
+        for (int s = 0; s < 16; ++s) sum += cnt[s];
+        if (sum != kTotalFreq && v->V.entropy) return fail(CSV_E_FORMAT, "counts must sum to 4096, got %u", sum);
+        uint32_t slot = 0;
+        for (int s = 0; s < 16 && slot < kTotalFreq; ++s)
+            for (uint32_t j = 0; j < cnt[s] && slot < kTotalFreq; ++j, ++slot)
+                dtab_host[tb * 4096 + slot] = ((uint32_t)cnt[s] << 16) | (j << 4) | (uint32_t)s;
+        for (; slot < kTotalFreq; ++slot) dtab_host[tb * 4096 + slot] = (1u << 16) | 0u;
+    }
+    return CSV_OK;
+}
+
+static void vol_release(csv_volume* v) {
+    if (!v) return;
+    cudaSetDevice(v->device);
+    cudaFree(v->d_soa); cudaFree(v->d_blob); cudaFree(v->d_dtab);
+    cudaFree(v->d_sizes); cudaFree(v->d_eoff); cudaFree(v->d_scan); cudaFree(v->d_sres);
+    cudaFree(v->d_counter); cudaFree(v->d_entries); cudaFree(v->d_gws);
+    delete v;
+}
+
+static int ensure_plan(csv_volume* v, uint64_t n, uint64_t entries_need, int Lg, cudaStream_t st) {
+    if (n > v->plan_cap) {
+        uint64_t cap = std::max<uint64_t>(n, 1024);
+        cudaFree(v->d_sizes); cudaFree(v->d_eoff); cudaFree(v->d_sres);
+        v->d_sizes = nullptr; v->d_eoff = nullptr; v->d_sres = nullptr; v->plan_cap = 0;
+        CUDA_TRY(cudaMalloc(&v->d_sizes, 2 * cap * sizeof(uint64_t)));
+        CUDA_TRY(cudaMalloc(&v->d_eoff, (2 * cap + 1) * sizeof(uint64_t)));
+        CUDA_TRY(cudaMalloc(&v->d_sres, 2 * cap * sizeof(csv_stream_result)));
+        v->plan_cap = cap;
+    }
+    if (!v->d_scan) {
+        CUDA_TRY(cudaMalloc(&v->d_scan, 4104 * sizeof(uint64_t)));
+        CUDA_TRY(cudaMalloc(&v->d_counter, sizeof(unsigned long long)));
+    }
+    if (entries_need + 64 > v->entries_cap) {
+        cudaStreamSynchronize(st);
+        cudaFree(v->d_entries);
+        v->d_entries = nullptr;
+        v->entries_cap = 0;
+        uint64_t cap = entries_need + 64;
+        CUDA_TRY(cudaMalloc(&v->d_entries, cap));
+        v->entries_cap = cap;
+    }
+    if (Lg > 5) {
+        uint64_t words = (uint64_t)k2_smem_bytes(Lg) / 4;
+        words = (words + 31) & ~31ull;
+        int ctas = v->nsm * 2;
+        if (words * ctas > v->gws_words_cap) {
+            cudaStreamSynchronize(st);
+            cudaFree(v->d_gws);
+            v->d_gws = nullptr;
+            CUDA_TRY(cudaMalloc(&v->d_gws, words * ctas * 4));
+            v->gws_words_cap = words * ctas;
+        }
+        v->gws_stride = words;
+        v->gws_ctas = ctas;
+    }
+    return CSV_OK;
+}
+
+static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, bool dir_on_device,
+                      uint64_t brick_begin, uint64_t brick_end,
+                      const uint32_t* palette, uint64_t palette_base, uint64_t palette_len,
+                      const uint8_t* coarse, uint64_t coarse_base, uint64_t coarse_len,
+                      const uint8_t* detail, uint64_t detail_base, uint64_t detail_len,
+                      bool blobs_on_device, uintptr_t stream, csv_volume** out) {
+    if (!head120 || !out) return fail(CSV_E_ARG, "null argument");
+    if (brick_end < brick_begin) return fail(CSV_E_ARG, "brick_end < brick_begin");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    csv_volume* v = new csv_volume();
+    v->device = device;
+    std::vector<uint32_t> dtab(8192);
+    int rc = parse_head(head120, v, dtab.data());
+    if (rc != CSV_OK) { delete v; return rc; }
+    uint64_t ntot = (uint64_t)(v->grid[0] * v->grid[1] * v->grid[2]);
+    if (brick_end > ntot) { delete v; return fail(CSV_E_ARG, "brick range [%llu, %llu) exceeds %llu bricks",
+                                                  (unsigned long long)brick_begin, (unsigned long long)brick_end,
+                                                  (unsigned long long)ntot); }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    v->nsm = nsm;
+    uint64_t n = brick_end - brick_begin;
+    v->V.brick_begin = brick_begin;
+    v->V.nb = n;
+    // directory SoA
+    size_t soa_bytes = n * (8 + 4 + 8 + 4 + 4 + 8 + 4 + 4) + 64;
+    cudaError_t ce = cudaMalloc(&v->d_soa, soa_bytes);
+    if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "directory: %s", cudaGetErrorString(ce)); }
+    uint8_t* p = (uint8_t*)v->d_soa;
+    uint64_t* pal_off = (uint64_t*)p; p += 8 * n;
+    uint64_t* c_off = (uint64_t*)p; p += 8 * n;
+    uint64_t* d_off = (uint64_t*)p; p += 8 * n;
+    uint32_t* pal_n = (uint32_t*)p; p += 4 * n;
+    uint32_t* c_bytes = (uint32_t*)p; p += 4 * n;
+    uint32_t* c_nib = (uint32_t*)p; p += 4 * n;
+    uint32_t* d_bytes = (uint32_t*)p; p += 4 * n;
+    uint32_t* d_nib = (uint32_t*)p; p += 4 * n;
+    v->V.pal_off = pal_off; v->V.pal_len = pal_n; v->V.c_off = c_off; v->V.c_bytes = c_bytes;
+    v->V.c_nib = c_nib; v->V.d_off = d_off; v->V.d_bytes = d_bytes; v->V.d_nib = d_nib;
+    // blobs
+    if (blobs_on_device) {
+        v->V.palette = palette;
+        v->V.coarse = coarse;
+        v->V.detail = detail;
+    } else {
+        uint64_t pb = ((palette_len * 4 + 15) & ~15ull) + 16;
+        uint64_t cb = ((coarse_len + 15) & ~15ull) + 16;
+        uint64_t db = ((detail_len + 15) & ~15ull) + 16;
+        ce = cudaMalloc(&v->d_blob, pb + cb + db);
+        if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "blobs: %s", cudaGetErrorString(ce)); }
+        cudaMemsetAsync(v->d_blob, 0, pb + cb + db, st);
+        if (palette_len) cudaMemcpyAsync(v->d_blob, palette, palette_len * 4, cudaMemcpyHostToDevice, st);
+        if (coarse_len) cudaMemcpyAsync(v->d_blob + pb, coarse, coarse_len, cudaMemcpyHostToDevice, st);
+        if (detail_len) cudaMemcpyAsync(v->d_blob + pb + cb, detail, detail_len, cudaMemcpyHostToDevice, st);
+        v->V.palette = (const uint32_t*)v->d_blob;
+        v->V.coarse = v->d_blob + pb;
+        v->V.detail = v->d_blob + pb + cb;
+    }
+    ce = cudaMalloc(&v->d_dtab, 8192 * 4);
+    if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "tables"); }
+    cudaMemcpyAsync(v->d_dtab, dtab.data(), 8192 * 4, cudaMemcpyHostToDevice, st);
+    v->V.dtab = v->d_dtab;
+    if (n) {
+        const uint8_t* ddir = dir44;
+        uint8_t* tmp = nullptr;
+        if (!dir_on_device) {
+            ce = cudaMalloc(&tmp, n * 44);
+            if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "directory staging"); }
+            cudaMemcpyAsync(tmp, dir44, n * 44, cudaMemcpyHostToDevice, st);
+            ddir = tmp;
+        }
+        k_unpack_dir<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ddir, n, palette_base, palette_len, coarse_base,
+                                                               coarse_len, detail_base, detail_len, pal_off, pal_n,
+                                                               c_off, c_bytes, c_nib, d_off, d_bytes, d_nib);
+        unsigned long long* stats = nullptr;
+        cudaMalloc(&stats, 16);
+        cudaMemsetAsync(stats, 0, 16, st);
+        k_region_stats<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v->V, stats, stats + 1);
+        unsigned long long hs[2] = {0, 0};
+        cudaMemcpyAsync(hs, stats, 16, cudaMemcpyDeviceToHost, st);
+        ce = cudaStreamSynchronize(st);
+        cudaFree(stats);
+        if (tmp) cudaFree(tmp);
+        if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_CUDA, "create: %s", cudaGetErrorString(ce)); }
+        v->region_total_t0 = hs[0];
+        v->region_max_t0 = hs[1];
+    }
+    *out = v;
+    return CSV_OK;
+}
+
+// ---------------------------------------------------------------------------- exported API
+extern "C" {
+
+int csv_version(void) { return 1; }
+const char* csv_last_error(void) { return g_err.c_str(); }
+
+int csv_volume_create(int device, const uint8_t* head120, const uint8_t* dir44, uint64_t brick_begin,
+                      uint64_t brick_end, const uint32_t* palette, uint64_t palette_base, uint64_t palette_len,
+                      const uint8_t* coarse, uint64_t coarse_base, uint64_t coarse_len, const uint8_t* detail,
+                      uint64_t detail_base, uint64_t detail_len, uintptr_t stream, csv_volume** vol) {
+    return vol_create(device, head120, dir44, false, brick_begin, brick_end, palette, palette_base, palette_len,
+                      coarse, coarse_base, coarse_len, detail, detail_base, detail_len, false, stream, vol);
+}
+
+int csv_volume_create_device(int device, const uint8_t* head120, const uint8_t* d_dir44, uint64_t brick_begin,
+                             uint64_t brick_end, const uint32_t* d_palette, uint64_t palette_base,
+                             uint64_t palette_len, const uint8_t* d_coarse, uint64_t coarse_base,
+                             uint64_t coarse_len, const uint8_t* d_detail, uint64_t detail_base,
+                             uint64_t detail_len, uintptr_t stream, csv_volume** vol) {
+    return vol_create(device, head120, d_dir44, true, brick_begin, brick_end, d_palette, palette_base, palette_len,
+                      d_coarse, coarse_base, coarse_len, d_detail, detail_base, detail_len, true, stream, vol);
+}
+
+int csv_volume_free(csv_volume* vol) {
+    vol_release(vol);
+    return CSV_OK;
+}
+
+int csv_volume_info(csv_volume* vol, int64_t* dims3, int64_t* grid3, int* brick_log2, int* entropy) {
+    if (!vol) return fail(CSV_E_ARG, "null volume");
+    if (dims3) memcpy(dims3, vol->dims, 24);
+    if (grid3) memcpy(grid3, vol->grid, 24);
+    if (brick_log2) *brick_log2 = vol->V.N;
+    if (entropy) *entropy = vol->V.entropy;
+    return CSV_OK;
+}
+
+int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, int64_t z_end, csv_result* d_res,
+                      uintptr_t stream) {
+    if (!vol || !d_out) return fail(CSV_E_ARG, "null argument");
+    if (t < 0 || t > vol->V.N) return fail(CSV_E_ARG, "LOD %d outside [0, %d]", t, vol->V.N);
+    CUDA_TRY(cudaSetDevice(vol->device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Plan P{};
+    P.n = vol->V.nb;
+    P.t_uniform = t;
+    P.out = d_out;
+    P.z_begin = z_begin;
+    P.z_end = z_end;
+    P.cx = (vol->dims[0] + (1ll << t) - 1) >> t;
+    P.cy = (vol->dims[1] + (1ll << t) - 1) >> t;
+    P.res = d_res;
+    if (t == vol->V.N) {
+        CUDA_TRY(csv::run_root_raster(vol->V, P, st));
+        return CSV_OK;
+    }
+    int rc = ensure_plan(vol, P.n, vol->region_total_t0, vol->V.N - t, st);
+    if (rc) return rc;
+    P.eoff = vol->d_eoff;
+    P.sres = vol->d_sres;
+    P.entries = vol->d_entries;
+    CUDA_TRY(run_decode(vol->V, P, 0, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
+                        vol->gws_ctas, vol->nsm, t, st));
+    return CSV_OK;
+}
+
+int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, const uint8_t* d_lod,
+                      const uint64_t* d_dst, uint32_t* d_pool, csv_result* d_res, uintptr_t stream) {
+    if (!vol || (n && (!d_brick || !d_lod || !d_dst || !d_pool))) return fail(CSV_E_ARG, "null argument");
+    if (n == 0) return CSV_OK;
+    CUDA_TRY(cudaSetDevice(vol->device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Plan P{};
+    P.n = n;
+    P.brick = d_brick;
+    P.lod = d_lod;
+    P.dst = d_dst;
+    P.out = d_pool;
+    P.res = d_res;
+    uint64_t need = n * vol->region_max_t0;
+    int rc = ensure_plan(vol, n, need, vol->V.N, st);
+    if (rc) return rc;
+    P.eoff = vol->d_eoff;
+    P.sres = vol->d_sres;
+    P.entries = vol->d_entries;
+    CUDA_TRY(run_decode(vol->V, P, 1, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
+                        vol->gws_ctas, vol->nsm, 0, st));
+    return CSV_OK;
+}
+
+int csv_streams_capacity(csv_volume* vol, uint64_t n, int t, uint64_t* cap) {
+    if (!vol || !cap) return fail(CSV_E_ARG, "null argument");
+    (void)t;
+    *cap = n * vol->region_max_t0 + 64;
+    return CSV_OK;
+}
+
+int csv_decode_streams(csv_volume* vol, uint64_t n, const uint32_t* d_brick, int t, uint8_t* d_entries,
+                       uint64_t entries_cap, uint64_t* d_entry_off, csv_stream_result* d_sres, uintptr_t stream) {
+    if (!vol || (n && (!d_entries || !d_entry_off || !d_sres))) return fail(CSV_E_ARG, "null argument");
+    if (t < 0 || t > vol->V.N) return fail(CSV_E_ARG, "LOD %d outside [0, %d]", t, vol->V.N);
+    if (n == 0) return CSV_OK;
+    if (entries_cap < n * vol->region_max_t0) return fail(CSV_E_ARG, "entries_cap too small (need %llu)",
+                                                          (unsigned long long)(n * vol->region_max_t0));
+    CUDA_TRY(cudaSetDevice(vol->device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int rc = ensure_plan(vol, n, 0, 0, st);
+    if (rc) return rc;
+    Plan P{};
+    P.n = n;
+    P.brick = d_brick;
+    P.t_uniform = t;
+    P.eoff = d_entry_off;
+    P.sres = d_sres;
+    P.entries = d_entries;
+    CUDA_TRY(run_streams_only(vol->V, P, vol->d_sizes, vol->d_scan, vol->d_counter, vol->nsm, st));
+    return CSV_OK;
+}
+
+}  // extern "C"

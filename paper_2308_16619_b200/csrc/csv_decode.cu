@@ -1,0 +1,892 @@
+// csv_decode.cu -- B200 (sm_100a) decode kernels for CSV compressed segmentation volumes.
+//
+// Hot path: per-brick decompression = rANS entropy decode +
+// coarse-to-fine operation replay, reference _decode_kernel
+// (/root/reference/pkg/src/csvol/codec.py:303-471).  Restructured for the GPU:
+//
+//  K1 k1_streams   -- entropy stage.  One LANE per (brick, stream): a lane owns
+//                     one single-state rANS chain (codec.py:290-300), decodes it
+//                     with the packed 4096-entry decode table in shared memory,
+//                     parses op/payload nibbles into one entry byte per
+//                     operation and stores them 8 at a time.  Lanes refill
+//                     work dynamically from a global counter (warp-aggregated
+//                     atomics), detail streams (long) first.
+//  K2 k2_replay    -- replay stage.  One CTA per brick, level-synchronous:
+//                     per level a popcount rank of active parents locates each
+//                     parent's 8 entries, a block scan of palette-advance
+//                     counts gives i_p, every child is evaluated independently
+//                     (same-level neighbour chains resolved directly, <=3
+//                     hops), and the final level streams straight to HBM in
+//                     raster (K3, decompress_volume) or Morton pool order (K4,
+//                     brick cache).
+#include <cstdio>
+#include <cstring>
+#include "csv_device.cuh"
+
+namespace csv {
+
+constexpr int K1_THREADS = 256;
+constexpr int K2_THREADS = 256;
+constexpr int K2_WARPS = K2_THREADS / 32;
+
+// ============================================================================ planning
+// Entry-region sizes per (request, stream) -> sizes[2r+s]; then exclusive scan.
+__global__ void k_region_sizes(VolView V, Plan P, uint64_t* sizes) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= 2 * P.n) return;
+    uint64_t r = i >> 1;
+    int s = (int)(i & 1);
+    uint64_t b = req_local(V, P, r);
+    int t = req_lod(P, r);
+    uint32_t lim = (b < V.nb && t < V.N) ? stream_limit(V, b, t, s) : 0;
+    sizes[i] = round16(lim);
+}
+
+// Simple 3-phase exclusive scan of u64 (n <= 4096 * 4096).
+constexpr int SCAN_ITEMS = 4096;
+__device__ __forceinline__ uint64_t warp_incl_scan(uint64_t v) {
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) >= o) v += u;
+    }
+    return v;
+}
+// Block-wide exclusive scan of one value per thread (blockDim multiple of 32, <= 1024).
+__device__ uint64_t block_excl_scan(uint64_t v, uint64_t* sh, uint64_t* total) {
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint64_t inc = warp_incl_scan(v);
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        uint64_t w = lane < nw ? sh[lane] : 0;
+        uint64_t wi = warp_incl_scan(w);
+        if (lane < nw) sh[lane] = wi - w;
+        if (lane == nw - 1) sh[32] = wi;
+    }
+    __syncthreads();
+    uint64_t r = sh[wid] + inc - v;
+    if (total) *total = sh[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void k_scan_blocks(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* block_sums) {
+    __shared__ uint64_t sh[33];
+    uint64_t base = (uint64_t)blockIdx.x * SCAN_ITEMS;
+    constexpr int PER = SCAN_ITEMS / 256;
+    uint64_t loc[PER];
+    uint64_t sum = 0;
+    for (int k = 0; k < PER; ++k) {
+        uint64_t i = base + threadIdx.x * PER + k;
+        loc[k] = i < n ? in[i] : 0;
+        sum += loc[k];
+    }
+    uint64_t tot;
+    uint64_t pre = block_excl_scan(sum, sh, &tot);
+    for (int k = 0; k < PER; ++k) {
+        uint64_t i = base + threadIdx.x * PER + k;
+        if (i < n) out[i] = pre;
+        pre += loc[k];
+    }
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+__global__ void k_scan_sums(uint64_t* block_sums, int nblocks, uint64_t* out_total) {
+    __shared__ uint64_t sh[33];
+    // nblocks <= 4096; 1024 threads x 4
+    uint64_t loc[4];
+    uint64_t sum = 0;
+    for (int k = 0; k < 4; ++k) {
+        int i = threadIdx.x * 4 + k;
+        loc[k] = i < nblocks ? block_sums[i] : 0;
+        sum += loc[k];
+    }
+    uint64_t tot;
+    uint64_t pre = block_excl_scan(sum, sh, &tot);
+    for (int k = 0; k < 4; ++k) {
+        int i = threadIdx.x * 4 + k;
+        if (i < nblocks) block_sums[i] = pre;
+        pre += loc[k];
+    }
+    if (threadIdx.x == 0) *out_total = tot;
+}
+__global__ void k_scan_add(uint64_t* out, uint64_t n, const uint64_t* block_sums) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] += block_sums[i / SCAN_ITEMS];
+}
+
+// ============================================================================ K1: entropy lanes
+// Per-lane stream state.  The byte reader keeps a 64-bit MSB-first bit buffer
+// (renorm bytes are consumed in stream order, rans.py:9-11) plus one aligned
+// 32-bit word in flight, so each refill's load latency overlaps ~6 symbols.
+struct Lane {
+    const uint32_t* wp;     // next aligned word to prefetch
+    uint64_t buf;           // upcoming stream bits, MSB first
+    uint64_t acc;           // pending entry bytes (<= 8)
+    uint64_t* outp;         // entry region (8-byte groups)
+    const uint8_t* rawp;    // raw mode: packed nibble bytes
+    uint32_t nxt;           // prefetched word
+    uint32_t x;             // rANS state (fits 32 bits: f*(x>>12) < 2^32)
+    uint32_t pos, len;      // bytes consumed (incl. 4 state bytes) / stream bytes
+    uint32_t i, lim, n;     // nibble index, nibble limit, stored count
+    uint32_t g;             // groups stored
+    uint32_t cur;           // current entry byte
+    uint64_t item;
+    int nb;                 // valid bits in buf
+    int k;                  // entries in acc
+    int tsel;               // decode table (0 interior, 1 leaf)
+    bool pend;              // next nibble is a P_delta payload
+    bool slow;              // first step from a state < 2^23 (corrupt streams only)
+};
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+
+__device__ __forceinline__ void lane_refill(Lane& L) {
+    L.buf |= (uint64_t)bswap32(L.nxt) << (32 - L.nb);
+    L.nb += 32;
+    L.nxt = __ldg(L.wp);
+    ++L.wp;
+}
+
+__device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
+    bool pay = L.pend;
+    L.pend = !pay && ((s & 7u) == 5u);
+    L.cur = pay ? (L.cur | (s << 4)) : s;
+    if (!L.pend) {
+        L.acc |= (uint64_t)L.cur << (8 * L.k);
+        if (++L.k == 8) {
+            L.outp[L.g++] = L.acc;
+            L.acc = 0;
+            L.k = 0;
+        }
+    }
+}
+
+__device__ __forceinline__ void lane_finish(Lane& L, const Plan& P, bool failed, bool entropy) {
+    if (L.k > 0) L.outp[L.g] = L.acc;
+    csv_stream_result r;
+    r.n_entries = L.g * 8 + L.k;
+    r.flags = 0;
+    r.fail_nibble = 0xffffffffu;
+    r.partial_op = 0;
+    if (failed) {
+        r.flags |= CSV_SF_FAILED;
+        r.fail_nibble = L.i;
+    } else if (L.i == L.n) {
+        r.flags |= CSV_SF_FAILED | CSV_SF_COMPLETE;
+        r.fail_nibble = L.n;
+        if (entropy && L.n > 0 && (L.x != kStateLower || L.pos != L.len)) r.flags |= CSV_SF_DESYNC;
+    }
+    if (L.pend) {
+        r.flags |= CSV_SF_PARTIAL;
+        r.partial_op = L.cur;
+    }
+    P.sres[L.item] = r;
+}
+
+// Initialise lane for work item `item`; returns false if the item finished at once.
+template <bool ENTROPY>
+__device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t item) {
+    uint64_t r = item < P.n ? item : item - P.n;
+    int s = item < P.n ? 1 : 0;           // detail streams first (longest chains)
+    uint64_t w = 2 * r + s;               // result / region index
+    L.item = w;
+    L.acc = 0; L.k = 0; L.g = 0; L.pend = false; L.cur = 0; L.i = 0; L.slow = false;
+    L.x = 0; L.pos = 0; L.len = 0; L.nb = 0; L.buf = 0;
+    uint64_t b = req_local(V, P, r);
+    int t = req_lod(P, r);
+    L.outp = reinterpret_cast<uint64_t*>(P.entries + P.eoff[w]);
+    bool ok = b < V.nb && t < V.N && !(s == 1 && t != 0);
+    L.n = ok ? eff_nibbles(V, b, s) : 0;
+    L.lim = ok ? stream_limit(V, b, t, s) : 0;
+    L.tsel = s;
+    if (!ok) {
+        L.n = 0; L.lim = 0;
+        P.sres[w] = csv_stream_result{0, 0xffffffffu, 0, 0};
+        return false;
+    }
+    const uint8_t* base = s ? V.detail + V.d_off[b] : V.coarse + V.c_off[b];
+    L.len = s ? V.d_bytes[b] : V.c_bytes[b];
+    if (L.lim == 0) {
+        if (L.n == 0) P.sres[w] = csv_stream_result{0, 0, CSV_SF_FAILED | CSV_SF_COMPLETE, 0};
+        else P.sres[w] = csv_stream_result{0, 0xffffffffu, 0, 0};
+        return false;
+    }
+    if (!ENTROPY) {
+        L.rawp = base;
+        return true;
+    }
+    if (L.len < 4) {   // entropy stream shorter than its state word (codec.py:333-334)
+        P.sres[w] = csv_stream_result{0, 0, CSV_SF_FAILED, 0};
+        return false;
+    }
+    L.x = (uint32_t)base[0] | ((uint32_t)base[1] << 8) | ((uint32_t)base[2] << 16) | ((uint32_t)base[3] << 24);
+    L.pos = 4;
+    uintptr_t q = reinterpret_cast<uintptr_t>(base) + 4;
+    const uint32_t* aq = reinterpret_cast<const uint32_t*>(q & ~uintptr_t(3));
+    int sh = (int)(q & 3);
+    L.buf = (uint64_t)bswap32(__ldg(aq)) << (32 + 8 * sh);
+    L.nb = 32 - 8 * sh;
+    L.wp = aq + 1;
+    L.nxt = __ldg(L.wp);
+    ++L.wp;
+    L.slow = L.x < kStateLower;
+    return true;
+}
+
+// One symbol; returns false when the lane's item is finished.
+template <bool ENTROPY>
+__device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t* tab) {
+    uint32_t s;
+    if (ENTROPY) {
+        if (L.nb < 16) lane_refill(L);
+        uint32_t e = tab[(L.tsel << 12) | (L.x & (kTotalFreq - 1))];
+        s = e & 15u;
+        uint32_t xn = (e >> 16) * (L.x >> kPrecision) + ((e >> 4) & 0xFFFu);
+        if (!L.slow) {
+            // after a step from x >= 2^23, x >= 2^11: at most two renorm bytes
+            uint32_t r = (xn < kStateLower) + (xn < (1u << 15));
+            if (L.pos + r > L.len) {           // underrun (codec.py:295-297)
+                lane_finish(L, P, true, true);
+                return false;
+            }
+            uint32_t top = (uint32_t)(L.buf >> 48);
+            L.x = (xn << (8 * r)) | (top >> (16 - 8 * r));
+            L.buf <<= 8 * r;
+            L.nb -= 8 * r;
+            L.pos += r;
+        } else {
+            L.slow = false;
+            while (xn < kStateLower) {
+                if (L.pos >= L.len) {
+                    lane_finish(L, P, true, true);
+                    return false;
+                }
+                if (L.nb < 8) lane_refill(L);
+                xn = (xn << 8) | (uint32_t)(L.buf >> 56);
+                L.buf <<= 8;
+                L.nb -= 8;
+                ++L.pos;
+            }
+            L.x = xn;
+        }
+    } else {
+        s = (L.rawp[L.i >> 1] >> (4 * (L.i & 1))) & 15u;
+    }
+    lane_emit(L, s);
+    if (++L.i == L.lim) {
+        lane_finish(L, P, false, ENTROPY);
+        return false;
+    }
+    return true;
+}
+
+template <bool ENTROPY>
+__global__ void __launch_bounds__(K1_THREADS) k1_streams(VolView V, Plan P, unsigned long long* counter) {
+    __shared__ uint32_t tab[2 * 4096];
+    if (ENTROPY) {
+        for (int i = threadIdx.x; i < 2 * 4096; i += blockDim.x) tab[i] = V.dtab[i];
+        __syncthreads();
+    }
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint64_t total = 2 * P.n;
+    Lane L;
+    bool has = false, done = false;
+    while (true) {
+        bool need = !has && !done;
+        unsigned m = __ballot_sync(FULL, need);
+        if (m) {
+            int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+            base = __shfl_sync(FULL, base, leader);
+            if (need) {
+                uint64_t my = base + __popc(m & ((1u << lane) - 1u));
+                if (my < total) has = lane_init<ENTROPY>(L, V, P, my);
+                else done = true;
+            }
+        }
+        if (__all_sync(FULL, done)) break;
+        if (has) {
+#pragma unroll 4
+            for (int u = 0; u < 32; ++u) {
+                if (!lane_step<ENTROPY>(L, P, tab)) { has = false; break; }
+            }
+        }
+    }
+}
+
+// ============================================================================ K2: replay
+// Shared (or global-workspace) layout for one brick, sized for L = N - t levels:
+//   lev  : values of levels t+1..N, Morton order, level k at levoff(N-k)
+//   mask : 2 x W words, active-parent bitmask ping-pong
+//   wpre : W words, exclusive popcount prefix of the parent mask
+//   ipb  : 8^(L-1) words, i_p at each active parent's first entry (by rank)
+struct Layout {
+    uint32_t lev, mask, wpre, ipb, words;   // offsets in u32 units
+};
+__host__ __device__ inline Layout make_layout(int L) {
+    Layout Y;
+    uint32_t nlev = 0;
+    for (int j = 0; j < L; ++j) nlev += 1u << (3 * j);
+    uint32_t maxP = 1u << (3 * (L - 1));
+    uint32_t W = (maxP + 31) / 32;
+    Y.lev = 0;
+    Y.mask = nlev;
+    Y.wpre = Y.mask + 2 * W;
+    Y.ipb = Y.wpre + W + 1;
+    Y.words = Y.ipb + maxP;
+    return Y;
+}
+__device__ __forceinline__ uint32_t levoff(int j) {   // j = N - level
+    return ((1u << (3 * j)) - 1u) / 7u;
+}
+
+enum { OUT_RASTER = 0, OUT_MORTON = 1 };
+
+// error key codes (low byte); the key orders by entry index first
+enum { EK_UNDERRUN_NV = 1, EK_BAD_OP = 2, EK_PAL_RANGE = 3, EK_DELTA_RANGE = 4, EK_BAD_NEIGHBOR = 6, EK_LEAF_STOP = 7 };
+
+struct K2Shared {
+    unsigned long long errkey;
+    uint32_t red[K2_WARPS + 1];
+    uint32_t scan[K2_WARPS + 1];
+    uint64_t red64[2][K2_WARPS];
+};
+
+// Block-wide in-place exclusive scan of arr[0..n) (u32), adding `base`; returns total.
+__device__ uint32_t block_scan_inplace(uint32_t* arr, uint32_t n, uint32_t base, K2Shared& S) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t per = (n + K2_WARPS - 1) / K2_WARPS;
+    uint32_t lo = wid * per, hi = min(n, lo + per);
+    uint32_t sum = 0;
+    for (uint32_t i = lo + lane; i < hi; i += 32) sum += arr[i];
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) S.scan[wid] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int w = 0; w < K2_WARPS; ++w) { uint32_t v = S.scan[w]; S.scan[w] = run; run += v; }
+        S.scan[K2_WARPS] = run;
+    }
+    __syncthreads();
+    uint32_t carry = base + S.scan[wid];
+    for (uint32_t c0 = lo; c0 < hi; c0 += 32) {
+        uint32_t i = c0 + lane;
+        uint32_t v = i < hi ? arr[i] : 0;
+        uint32_t inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (i < hi) arr[i] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    uint32_t total = S.scan[K2_WARPS];
+    __syncthreads();
+    return total;
+}
+
+__device__ __forceinline__ uint64_t block_sum64(uint64_t v, int slot, K2Shared& S) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) S.red64[slot][threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint64_t t = 0;
+    for (int w = 0; w < K2_WARPS; ++w) t += S.red64[slot][w];
+    __syncthreads();
+    return t;
+}
+
+// Per-level context for child evaluation.
+struct LevelCtx {
+    const uint32_t* plev;    // parent level values (Morton)
+    const uint32_t* pmask;   // parent active bitmask
+    const uint32_t* wpre;    // word rank prefix
+    const uint32_t* ipb;     // i_p base per active parent (by rank)
+    const uint64_t* E8;      // entry groups of this stream, group index = entry/8
+    uint32_t g0;             // first group of this level (e0 / 8)
+    uint32_t gcap;           // groups inside the stream's entry region
+    const uint32_t* pal;
+    uint32_t plen;
+    int cbits;               // bits per axis at the child level
+};
+
+__device__ __forceinline__ bool is_active(const LevelCtx& C, uint32_t q) {
+    return (C.pmask[q >> 5] >> (q & 31)) & 1u;
+}
+__device__ __forceinline__ uint32_t rank_of(const LevelCtx& C, uint32_t q) {
+    return C.wpre[q >> 5] + __popc(C.pmask[q >> 5] & ((1u << (q & 31)) - 1u));
+}
+__device__ __forceinline__ uint64_t load_group(const LevelCtx& C, uint32_t r) {
+    uint32_t g = C.g0 + r;
+    return g < C.gcap ? __ldg(C.E8 + g) : 0ull;
+}
+__device__ __forceinline__ uint32_t pal_at(const LevelCtx& C, int64_t idx) {
+    idx = idx < 0 ? 0 : idx;
+    idx = idx >= (int64_t)C.plen ? (int64_t)C.plen - 1 : idx;
+    return __ldg(C.pal + idx);
+}
+
+// Value of same-level node nm (already decoded in sequential order, nm < j):
+// inactive parent -> parent's value; otherwise evaluate its entry.  Each
+// even-coordinate hop makes one more coordinate odd, so <= 3 hops.
+__device__ uint32_t neighbor_value(const LevelCtx& C, uint32_t nm) {
+    for (int hop = 0; hop < 4; ++hop) {
+        uint32_t q = nm >> 3;
+        int c = nm & 7;
+        if (!is_active(C, q)) return C.plev[q];
+        uint32_t r = rank_of(C, q);
+        uint64_t w = load_group(C, r);
+        uint32_t e = (uint32_t)(w >> (8 * c)) & 0xFFu;
+        uint32_t op = e & 7u;
+        if (op == 0) return C.plev[q];
+        if (op <= 3) {
+            int a = op - 1;
+            uint32_t M = axis_mask(a, C.cbits);
+            uint32_t part = nm & M;
+            if ((c >> a) & 1) {                 // odd: +1 neighbour is decoded later -> its parent
+                if (part == M) return 0;        // outside brick (an earlier error)
+                uint32_t nn = (((part | ~M) + 1u) & M) | (nm & ~M);
+                return C.plev[nn >> 3];
+            }
+            if (part == 0) return 0;
+            nm = ((part - 1u) & M) | (nm & ~M);
+            continue;
+        }
+        if (op == 7) return 0;
+        int64_t ip = (int64_t)C.ipb[r] + prefix_bytes(op_eq(w, 6), c);
+        uint32_t d = e >> 4;
+        int64_t idx = op == 4 ? ip : (op == 5 ? ip - d - 1 : ip + 1);
+        return pal_at(C, idx);
+    }
+    return 0;
+}
+
+// Evaluate the 8 children of active parent q whose entries are `w`.
+// Errors are reported as (entry key) via errkey.
+__device__ __forceinline__ void eval_group(const LevelCtx& C, uint32_t q, uint64_t w, uint32_t r,
+                                           uint32_t e_first, uint32_t nvalid, bool leaf,
+                                           uint32_t* v, unsigned long long* errkey) {
+    const uint32_t pv = C.plev[q];
+    const uint64_t pa = op_eq(w, 6);
+    const uint32_t ipq = C.ipb[r];
+    unsigned long long myerr = ~0ull;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        uint32_t e = (uint32_t)(w >> (8 * c)) & 0xFFu;
+        uint32_t op = e & 7u;
+        uint32_t val = pv;
+        int code = 0;
+        if (op >= 1 && op <= 3) {
+            int a = op - 1;
+            uint32_t j = (q << 3) | c;
+            uint32_t M = axis_mask(a, C.cbits);
+            uint32_t part = j & M;
+            if ((c >> a) & 1) {
+                if (part == M) code = EK_BAD_NEIGHBOR;
+                else {
+                    uint32_t nn = (((part | ~M) + 1u) & M) | (j & ~M);
+                    val = C.plev[nn >> 3];
+                }
+            } else {
+                if (part == 0) code = EK_BAD_NEIGHBOR;
+                else val = neighbor_value(C, ((part - 1u) & M) | (j & ~M));
+            }
+        } else if (op >= 4 && op <= 6) {
+            int64_t ip = (int64_t)ipq + prefix_bytes(pa, c);
+            int64_t idx;
+            if (op == 4) idx = ip;
+            else if (op == 5) { idx = ip - (int64_t)(e >> 4) - 1; if (idx < 0) code = EK_DELTA_RANGE; }
+            else { idx = ip + 1; if (idx >= (int64_t)C.plen) code = EK_PAL_RANGE; }
+            val = pal_at(C, idx);
+        } else if (op == 7) {
+            code = EK_BAD_OP;
+        }
+        if (op != 7 && leaf && (e & 8u)) code = EK_LEAF_STOP;   // checked before the op (codec.py:396-399)
+        v[c] = val;
+        uint32_t ent = e_first + c;
+        if (code && ent < nvalid) {
+            unsigned long long key = ((unsigned long long)ent << 8) | (unsigned)code;
+            myerr = key < myerr ? key : myerr;
+        }
+    }
+    if (myerr != ~0ull) atomicMin(errkey, myerr);
+}
+
+// Final-level writer, raster (Z,Y,X) slab: children of parent (qx,qy,qz).
+__device__ __forceinline__ void store_raster(const Plan& P, int64_t ox, int64_t oy, int64_t oz,
+                                             const uint32_t* v) {
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz) {
+        int64_t z = oz + dz;
+        if (z < P.z_begin || z >= P.z_end) continue;
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+            int64_t y = oy + dy;
+            if (y >= P.cy) continue;
+            uint32_t* row = P.out + ((z - P.z_begin) * P.cy + y) * P.cx;
+            uint32_t a = v[dz * 4 + dy * 2], b = v[dz * 4 + dy * 2 + 1];
+            if (ox + 1 < P.cx) {
+                uint32_t* p = row + ox;
+                if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
+                else { p[0] = a; p[1] = b; }
+            } else if (ox < P.cx) {
+                row[ox] = a;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void store_morton(uint32_t* out, uint32_t q, const uint32_t* v, bool al16) {
+    uint32_t* p = out + 8ull * q;
+    if (al16) {
+        reinterpret_cast<uint4*>(p)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<uint4*>(p)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) p[c] = v[c];
+    }
+}
+
+__device__ __forceinline__ void write_result(const Plan& P, uint64_t r, int st, int stream, int64_t pos,
+                                             int64_t ci, int64_t di) {
+    if (P.res && threadIdx.x == 0) {
+        csv_result o;
+        o.status = st; o.stream = stream; o.pos = pos; o.ci = ci; o.di = di;
+        P.res[r] = o;
+    }
+}
+
+// Fill the whole output of request r with one value (relevant == 0, codec.py:353-358).
+template <int MODE>
+__device__ void fill_output(const VolView& V, const Plan& P, uint64_t b, int t, uint32_t* out_m, uint32_t val) {
+    int side = 1 << (V.N - t);
+    if (MODE == OUT_MORTON) {
+        uint64_t n = 1ull << (3 * (V.N - t));
+        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) out_m[i] = val;
+    } else {
+        int64_t bx = (int64_t)((V.brick_begin + b) % V.gx), by = (int64_t)(((V.brick_begin + b) / V.gx) % V.gy),
+                bz = (int64_t)((V.brick_begin + b) / (V.gx * V.gy));
+        uint64_t n = 1ull << (3 * (V.N - t));
+        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            int64_t x = i & (side - 1), y = (i >> (V.N - t)) & (side - 1), z = i >> (2 * (V.N - t));
+            int64_t gx = bx * side + x, gy = by * side + y, gz = bz * side + z;
+            if (gx < P.cx && gy < P.cy && gz >= P.z_begin && gz < P.z_end)
+                P.out[((gz - P.z_begin) * P.cy + gy) * P.cx + gx] = val;
+        }
+    }
+}
+
+template <int MODE, bool SMEM>
+__global__ void __launch_bounds__(K2_THREADS) k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
+    extern __shared__ __align__(16) uint32_t dsm[];
+    __shared__ K2Shared S;
+    const Layout Y = make_layout(Lmax);
+    uint32_t* ws = SMEM ? dsm : gws + blockIdx.x * ws_stride;
+    for (uint64_t r = blockIdx.x; r < P.n; r += gridDim.x) {
+        const uint64_t b = req_local(V, P, r);
+        const int t = req_lod(P, r);
+        const int N = V.N;
+        if (b >= V.nb || t > N) { write_result(P, r, -1, 0, 0, 0, 0); continue; }
+        // this variant handles N - t <= Lmax; others belong to the other launch
+        if (t < N && N - t > Lmax) continue;
+        if (!SMEM && N - t <= 5) continue;
+        uint32_t* out_m = MODE == OUT_MORTON ? P.out + P.dst[r] : nullptr;
+        const uint32_t plen = V.pal_len[b];
+        const uint32_t* pal = V.palette + V.pal_off[b];
+        if (plen == 0) { write_result(P, r, CSV_ST_EMPTY_PALETTE, 0, 0, 0, 0); continue; }
+        if (t == N) {   // coarsest LOD: palette[0] (codec.py:514-516, container.py:178-182)
+            if (threadIdx.x == 0) {
+                uint32_t v0 = __ldg(pal);
+                if (MODE == OUT_MORTON) out_m[0] = v0;
+                else fill_output<MODE>(V, P, b, t, nullptr, v0);
+            }
+            write_result(P, r, 0, 0, 0, 0, 0);
+            continue;
+        }
+        const uint32_t nc_raw = V.c_nib[b], nd_raw = t == 0 ? V.d_nib[b] : 0;
+        const uint32_t nc = eff_nibbles(V, b, 0), nd = t == 0 ? eff_nibbles(V, b, 1) : 0;
+        if (V.entropy) {   // state-word checks come first (codec.py:331-351)
+            if (nc_raw > 0 && V.c_bytes[b] < 4) { write_result(P, r, CSV_ST_UNDERRUN, 0, 0, 0, 0); continue; }
+            if (t == 0 && nd_raw > 0 && V.d_bytes[b] < 4) { write_result(P, r, CSV_ST_UNDERRUN, 1, 0, 0, 0); continue; }
+        }
+        if ((uint64_t)nc + nd == 0) {
+            fill_output<MODE>(V, P, b, t, out_m, __ldg(pal));
+            write_result(P, r, 0, 0, 0, 0, 0);
+            continue;
+        }
+        const csv_stream_result sr[2] = {P.sres[2 * r], P.sres[2 * r + 1]};
+        const uint64_t* E8[2] = {reinterpret_cast<const uint64_t*>(P.entries + P.eoff[2 * r]),
+                                 reinterpret_cast<const uint64_t*>(P.entries + P.eoff[2 * r + 1])};
+        const uint32_t gcap[2] = {(uint32_t)((P.eoff[2 * r + 1] - P.eoff[2 * r]) >> 3),
+                                  (uint32_t)((P.eoff[2 * r + 2] - P.eoff[2 * r + 1]) >> 3)};
+        uint32_t* lev = ws + Y.lev;
+        uint32_t* mask0 = ws + Y.mask;
+        const uint32_t Wmax = (Y.wpre - Y.mask) / 2;
+        uint32_t* wpre = ws + Y.wpre;
+        uint32_t* ipb = ws + Y.ipb;
+        if (threadIdx.x == 0) {
+            lev[0] = __ldg(pal);      // root (codec.py:353)
+            mask0[0] = 1u;
+            S.errkey = ~0ull;
+        }
+        __syncthreads();
+        uint32_t cursor[2] = {0, 0};
+        uint64_t pd_acc[2] = {0, 0};
+        uint32_t ipbase = 0;
+        int cur = 0;
+        bool failed = false;
+        int64_t bx = 0, by = 0, bz = 0;
+        if (MODE == OUT_RASTER) {
+            uint64_t gb = V.brick_begin + b;
+            bx = (int64_t)(gb % V.gx); by = (int64_t)((gb / V.gx) % V.gy); bz = (int64_t)(gb / (V.gx * V.gy));
+        }
+        for (int l = N; l > t; --l) {
+            const int s = l == 1 ? 1 : 0;
+            const bool leaf = l == 1;
+            const bool final_level = (l - 1 == t);
+            const uint32_t Pn = 1u << (3 * (N - l));
+            const uint32_t W = (Pn + 31) >> 5;
+            uint32_t* pmask = mask0 + cur * Wmax;
+            uint32_t* cmask = mask0 + (cur ^ 1) * Wmax;
+            // (A) rank prefix of active parents
+            for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
+                uint32_t mw = pmask[i];
+                if (Pn < 32) mw &= (1u << Pn) - 1u;
+                pmask[i] = mw;
+                wpre[i] = __popc(mw);
+            }
+            __syncthreads();
+            const uint32_t nact = block_scan_inplace(wpre, W, 0, S);
+            // (B) palette-advance counts per active parent, scanned into i_p bases
+            LevelCtx C;
+            C.plev = lev + levoff(N - l);
+            C.pmask = pmask;
+            C.wpre = wpre;
+            C.ipb = ipb;
+            C.E8 = E8[s];
+            C.g0 = cursor[s] >> 3;
+            C.gcap = gcap[s];
+            C.pal = pal;
+            C.plen = plen;
+            C.cbits = N - l + 1;
+            uint64_t pdl = 0;
+            for (uint32_t i = threadIdx.x; i < nact; i += blockDim.x) {
+                uint64_t w = load_group(C, i);
+                ipb[i] = __popcll(op_eq(w, 6));
+                pdl += __popcll(op_eq(w, 5));
+            }
+            pd_acc[s] += pdl;
+            __syncthreads();
+            const uint32_t tot_pa = block_scan_inplace(ipb, nact, ipbase, S);
+            const uint32_t nvalid = sr[s].n_entries;
+            const uint32_t e0 = cursor[s];
+            // (C) evaluate children
+            uint32_t* clev = final_level ? nullptr : lev + levoff(N - l + 1);
+            if (final_level && MODE == OUT_RASTER) {
+                const int pb = N - l;   // bits per axis at the parent level
+                const int64_t side_t = 1ll << (N - t);
+                for (uint32_t i = threadIdx.x; i < Pn; i += blockDim.x) {
+                    uint32_t qx = i & ((1u << pb) - 1u), qy = (i >> pb) & ((1u << pb) - 1u), qz = i >> (2 * pb);
+                    uint32_t q = spread3_u32(qx) | (spread3_u32(qy) << 1) | (spread3_u32(qz) << 2);
+                    uint32_t v[8];
+                    if (is_active(C, q)) {
+                        uint32_t rk = rank_of(C, q);
+                        uint64_t w = load_group(C, rk);
+                        eval_group(C, q, w, rk, e0 + 8 * rk, nvalid, leaf, v, &S.errkey);
+                    } else {
+                        uint32_t pv = C.plev[q];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) v[c] = pv;
+                    }
+                    store_raster(P, bx * side_t + 2 * qx, by * side_t + 2 * qy, bz * side_t + 2 * qz, v);
+                }
+            } else {
+                const bool al16 = MODE == OUT_MORTON && ((reinterpret_cast<uintptr_t>(out_m) & 15) == 0);
+                for (uint32_t q = threadIdx.x; q < Pn; q += blockDim.x) {
+                    uint32_t v[8];
+                    uint32_t cm = 0;
+                    if (is_active(C, q)) {
+                        uint32_t rk = rank_of(C, q);
+                        uint64_t w = load_group(C, rk);
+                        eval_group(C, q, w, rk, e0 + 8 * rk, nvalid, leaf, v, &S.errkey);
+                        // stop bits -> inactive children (codec.py:460-463); packed to one byte
+                        uint64_t st = (w >> 3) & 0x0101010101010101ull;
+                        cm = (~(uint32_t)((st * 0x0102040810204080ull) >> 56)) & 0xFFu;
+                    } else {
+                        uint32_t pv = C.plev[q];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) v[c] = pv;
+                    }
+                    if (final_level) {
+                        store_morton(out_m, q, v, al16);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) clev[8 * q + c] = v[c];
+                        reinterpret_cast<uint8_t*>(cmask)[q] = (uint8_t)cm;
+                    }
+                }
+            }
+            if (threadIdx.x == 0 && (uint64_t)e0 + 8ull * nact > nvalid) {
+                unsigned long long key = ((unsigned long long)nvalid << 8) | EK_UNDERRUN_NV;
+                atomicMin(&S.errkey, key);
+            }
+            __syncthreads();
+            const unsigned long long ek = S.errkey;
+            if (ek != ~0ull) {
+                // first failing entry in sequential order -> status + nibble position
+                const uint32_t ent = (uint32_t)(ek >> 8);
+                const int code = (int)(ek & 0xFF);
+                int st;
+                int64_t pos;
+                if (code == EK_UNDERRUN_NV) {
+                    const csv_stream_result& q = sr[s];
+                    if ((q.flags & CSV_SF_PARTIAL) && leaf && (q.partial_op & 8u)) {
+                        st = CSV_ST_LEAF_STOP;
+                        pos = (int64_t)q.fail_nibble - 1;
+                    } else {
+                        st = CSV_ST_UNDERRUN;
+                        pos = (q.flags & CSV_SF_FAILED) ? (int64_t)q.fail_nibble : (int64_t)ent;
+                    }
+                } else {
+                    // nibble index of entry `ent` = ent + #payload nibbles before it
+                    uint64_t cnt = 0;
+                    for (uint32_t g = threadIdx.x; g < (ent + 7) / 8; g += blockDim.x) {
+                        uint64_t w = (g < gcap[s]) ? __ldg(E8[s] + g) : 0ull;
+                        uint32_t lim = ent - 8 * g;
+                        if (lim < 8) w &= (1ull << (8 * lim)) - 1ull;
+                        cnt += __popcll(op_eq(w, 5) & ((lim < 8) ? ((1ull << (8 * lim)) - 1ull) : ~0ull));
+                    }
+                    pos = (int64_t)ent + (int64_t)block_sum64(cnt, 0, S);
+                    st = code;
+                    if (code == EK_DELTA_RANGE) pos += 1;   // reported at the payload nibble
+                }
+                write_result(P, r, st, s, pos, 0, 0);
+                failed = true;
+                break;
+            }
+            cursor[s] = e0 + 8 * nact;
+            ipbase += tot_pa;
+            cur ^= 1;
+        }
+        if (!failed) {
+            const int64_t pdc = (int64_t)block_sum64(pd_acc[0], 0, S);
+            const int64_t pdd = (int64_t)block_sum64(pd_acc[1], 1, S);
+            const int64_t ci = (int64_t)cursor[0] + pdc, di = (int64_t)cursor[1] + pdd;
+            int st = 0, stream = 0;
+            int64_t pos = 0;
+            if (V.entropy) {   // full consumption must land on the initial state (codec.py:464-470)
+                if (nc_raw > 0 && ci == (int64_t)nc_raw && (sr[0].flags & CSV_SF_DESYNC)) { st = CSV_ST_DESYNC; stream = 0; pos = ci; }
+                else if (t == 0 && nd_raw > 0 && di == (int64_t)nd_raw && (sr[1].flags & CSV_SF_DESYNC)) { st = CSV_ST_DESYNC; stream = 1; pos = di; }
+            }
+            write_result(P, r, st, stream, pos, ci, di);
+        }
+        __syncthreads();
+    }
+}
+
+// Coarsest-LOD raster (t == N): one voxel per brick.
+__global__ void k_root_raster(VolView V, Plan P) {
+    uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (b >= V.nb) return;
+    uint32_t plen = V.pal_len[b];
+    if (P.res) {
+        csv_result o{plen == 0 ? CSV_ST_EMPTY_PALETTE : 0, 0, 0, 0, 0};
+        P.res[b] = o;
+    }
+    if (plen == 0) return;
+    uint64_t gb = V.brick_begin + b;
+    int64_t x = gb % V.gx, y = (gb / V.gx) % V.gy, z = gb / (V.gx * V.gy);
+    if (x < P.cx && y < P.cy && z >= P.z_begin && z < P.z_end)
+        P.out[((z - P.z_begin) * P.cy + y) * P.cx + x] = V.palette[V.pal_off[b]];
+}
+
+// ============================================================================ host launchers
+template <bool E>
+static void launch_k1(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
+    uint64_t items = 2 * P.n;
+    uint64_t want = (items + 31) / 32;                 // warps needed at one item per lane
+    uint64_t blocks = (want + K1_THREADS / 32 - 1) / (K1_THREADS / 32);
+    uint64_t cap = (uint64_t)nsm * 8;                  // 8 x 256 threads per SM resident (32 KB smem each)
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    k1_streams<E><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
+}
+
+}  // namespace csv
+
+// ---------------------------------------------------------------------------- internal host API
+namespace csv {
+
+struct Runtime {
+    int nsm = 148;
+};
+
+cudaError_t run_scan(const uint64_t* sizes, uint64_t* out, uint64_t n, uint64_t* tmp, cudaStream_t st) {
+    // out has n+1 slots; tmp >= nblocks + 1 slots
+    uint64_t nblocks = (n + SCAN_ITEMS - 1) / SCAN_ITEMS;
+    if (nblocks == 0) nblocks = 1;
+    if (nblocks > 4096) return cudaErrorInvalidValue;
+    k_scan_blocks<<<(unsigned)nblocks, 256, 0, st>>>(sizes, out, n, tmp);
+    k_scan_sums<<<1, 1024, 0, st>>>(tmp, (int)nblocks, out + n);
+    k_scan_add<<<(unsigned)((n + 255) / 256 ? (n + 255) / 256 : 1), 256, 0, st>>>(out, n, tmp);
+    return cudaGetLastError();
+}
+
+size_t k2_smem_bytes(int L) { return (size_t)make_layout(L).words * 4; }
+
+// Decode a plan: sizes -> scan -> K1 -> K2.  Workspace pointers are provided by the caller.
+cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, uint64_t* scan_tmp,
+                       unsigned long long* counter, uint32_t* gws, uint64_t gws_stride, int gws_ctas,
+                       int nsm, int min_t, cudaStream_t st) {
+    if (P.n == 0) return cudaSuccess;
+    unsigned nb = (unsigned)((2 * P.n + 255) / 256);
+    k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
+    cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
+    else launch_k1<false>(V, P, counter, nsm, st);
+    // K2 smem variant (N - t <= 5)
+    int Ls = V.N - min_t;
+    if (Ls > 5) Ls = 5;
+    if (Ls < 1) Ls = 1;
+    size_t smem = k2_smem_bytes(Ls);
+    unsigned grid = (unsigned)(P.n < 0x7fffffffull ? P.n : 0x7fffffffull);
+    if (mode == OUT_RASTER) {
+        cudaFuncSetAttribute(k2_replay<OUT_RASTER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k2_replay<OUT_RASTER, true><<<grid, K2_THREADS, smem, st>>>(V, P, Ls, nullptr, 0);
+    } else {
+        cudaFuncSetAttribute(k2_replay<OUT_MORTON, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k2_replay<OUT_MORTON, true><<<grid, K2_THREADS, smem, st>>>(V, P, Ls, nullptr, 0);
+    }
+    if (V.N - min_t > 5 && gws) {
+        unsigned g = (unsigned)(P.n < (uint64_t)gws_ctas ? P.n : (uint64_t)gws_ctas);
+        int Lg = V.N - min_t;
+        if (mode == OUT_RASTER) k2_replay<OUT_RASTER, false><<<g, K2_THREADS, 0, st>>>(V, P, Lg, gws, gws_stride);
+        else k2_replay<OUT_MORTON, false><<<g, K2_THREADS, 0, st>>>(V, P, Lg, gws, gws_stride);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t run_root_raster(const VolView& V, Plan P, cudaStream_t st) {
+    unsigned nb = (unsigned)((V.nb + 255) / 256);
+    if (nb == 0) return cudaSuccess;
+    k_root_raster<<<nb, 256, 0, st>>>(V, P);
+    return cudaGetLastError();
+}
+
+cudaError_t run_streams_only(const VolView& V, Plan P, uint64_t* sizes_tmp, uint64_t* scan_tmp,
+                             unsigned long long* counter, int nsm, cudaStream_t st) {
+    if (P.n == 0) return cudaSuccess;
+    unsigned nb = (unsigned)((2 * P.n + 255) / 256);
+    k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
+    cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
+    else launch_k1<false>(V, P, counter, nsm, st);
+    return cudaGetLastError();
+}
+
+}  // namespace csv

@@ -1,0 +1,117 @@
+// csv_device.cuh -- shared device-side types and helpers for the B200 CSV decoder.
+//
+// Data layout in HBM: the container's directory is unpacked
+// once into SoA columns (local brick index), the three blobs stay exactly as
+// in the CSV1 file (palette u32, coarse bytes, detail bytes) plus 16 B of
+// tail padding so the entropy lanes may prefetch one word past a stream.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/csvgpu.h"
+
+namespace csv {
+
+constexpr uint32_t kStateLower = 1u << 23;   // rans.py:27
+constexpr int kPrecision = 12;               // rans.py:25
+constexpr uint32_t kTotalFreq = 1u << 12;    // rans.py:26
+
+// Read-only view of one uploaded volume (bricks [brick_begin, brick_begin + nb)).
+struct VolView {
+    const uint64_t* pal_off;   // rebased to the uploaded palette slice (entries)
+    const uint32_t* pal_len;   // clamped like numpy slicing
+    const uint64_t* c_off;
+    const uint32_t* c_bytes;
+    const uint32_t* c_nib;
+    const uint64_t* d_off;
+    const uint32_t* d_bytes;
+    const uint32_t* d_nib;
+    const uint32_t* palette;
+    const uint8_t* coarse;
+    const uint8_t* detail;
+    const uint32_t* dtab;      // 2 x 4096 packed decode tables (interior, leaf)
+    int N;                     // brick_log2
+    int entropy;               // header flag bit 0 (container.py:7)
+    int64_t X, Y, Z;           // original dims
+    int64_t gx, gy, gz;        // brick grid
+    uint64_t brick_begin;
+    uint64_t nb;
+};
+
+// One decode call: n requests; request r decodes brick `brick[r]` at LOD lod[r].
+struct Plan {
+    uint64_t n;
+    const uint32_t* brick;     // global brick index, or nullptr => brick_begin + r
+    const uint8_t* lod;        // per-request LOD, or nullptr => t_uniform
+    int t_uniform;
+    const uint64_t* dst;       // Morton mode: pool element offset per request
+    uint32_t* out;             // raster slab base or pool base
+    int64_t z_begin, z_end;    // raster slab (LOD-t voxel rows)
+    int64_t cx, cy;            // cropped LOD-t x/y extent
+    uint64_t* eoff;            // [2n+1] entry-region offsets (bytes)
+    csv_stream_result* sres;   // [2n]
+    uint8_t* entries;
+    csv_result* res;           // [n] or nullptr
+};
+
+__device__ __forceinline__ uint64_t req_local(const VolView& V, const Plan& P, uint64_t r) {
+    return P.brick ? (uint64_t)P.brick[r] - V.brick_begin : r;
+}
+__device__ __forceinline__ int req_lod(const Plan& P, uint64_t r) {
+    return P.lod ? (int)P.lod[r] : P.t_uniform;
+}
+
+// Max entries the replay can consume from a stream (coarse: levels N..max(t+1,2);
+// detail: level 1 when t == 0).  Entries are at most 2 nibbles (codec.py:203-211),
+// so K1 never needs more than 2x this many nibbles (prefix decode, codec.py:330).
+__host__ __device__ __forceinline__ uint32_t max_entries(int N, int t, int s) {
+    if (s == 1) return t == 0 ? (1u << (3 * N)) : 0u;
+    uint32_t tot = 0;
+    int lo = t + 1 > 2 ? t + 1 : 2;
+    for (int l = N; l >= lo; --l) tot += 1u << (3 * (N - l + 1));
+    return tot;
+}
+
+// Effective nibble count: raw containers unpack 2 nibbles/byte and slice to the
+// stored count (container.py:333-337), so the count saturates at 2*bytes.
+__device__ __forceinline__ uint32_t eff_nibbles(const VolView& V, uint64_t b, int s) {
+    uint32_t n = s ? V.d_nib[b] : V.c_nib[b];
+    if (!V.entropy) {
+        uint64_t cap = 2ull * (s ? V.d_bytes[b] : V.c_bytes[b]);
+        if (n > cap) n = (uint32_t)cap;
+    }
+    return n;
+}
+
+__device__ __forceinline__ uint32_t stream_limit(const VolView& V, uint64_t b, int t, int s) {
+    if (s == 1 && t != 0) return 0;
+    uint32_t n = eff_nibbles(V, b, s);
+    uint32_t cap = 2u * max_entries(V.N, t, s);
+    return n < cap ? n : cap;
+}
+
+__host__ __device__ __forceinline__ uint64_t round16(uint64_t v) { return (v + 15) & ~15ull; }
+
+// ---- Morton (x lowest bit, morton.py:3-6) on brick-local indices (<= 21 bits)
+__device__ __forceinline__ uint32_t axis_mask(int a, int bits_per_axis) {
+    uint32_t m = 0x49249u << a;                   // bits a, a+3, ..., a+18
+    return m & ((1u << (3 * bits_per_axis)) - 1u);
+}
+__device__ __forceinline__ uint32_t spread3_u32(uint32_t v) {   // 7-bit coordinate -> bits 0,3,..,18
+    v = (v | (v << 8)) & 0x0000F00Fu;
+    v = (v | (v << 4)) & 0x000C30C3u;
+    v = (v | (v << 2)) & 0x00249249u;
+    return v;
+}
+
+// ---- SWAR helpers over 8 entry bytes (entry = op | stop<<3 | delta<<4)
+__device__ __forceinline__ uint64_t op_eq(uint64_t w, uint32_t op) {
+    const uint64_t ones = 0x0101010101010101ull;
+    uint64_t d = (w & 0x0707070707070707ull) ^ (ones * op);
+    uint64_t nz = (d | (d >> 1) | (d >> 2)) & ones;
+    return nz ^ ones;   // 0x01 in every byte whose op == `op`
+}
+__device__ __forceinline__ uint32_t prefix_bytes(uint64_t m, int c) {   // # flagged bytes before byte c
+    return (uint32_t)__popcll(m & ((1ull << (8 * c)) - 1ull));
+}
+
+}  // namespace csv

@@ -1,0 +1,199 @@
+"""Device-resident volumes: the Python side of the C-ABI decode path.
+
+`GpuVolume` owns one `csv_volume` handle (include/csvgpu.h): the container's
+directory, palette/coarse/detail blobs and decode tables uploaded to HBM,
+plus the decode workspace.  PyTorch provides device buffers and streams only;
+all decode work runs in libcsvgpu.so's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import CorruptStreamError
+
+ERROR_TEXT = {   # codec.py:487-495
+    1: "stream underrun",
+    2: "invalid opcode 7",
+    3: "palette index out of range",
+    4: "palette back-reference before palette start",
+    5: "entropy stream desynchronized",
+    6: "neighbor reference outside the brick",
+    7: "stop bit set on a leaf-level entry",
+}
+STREAM_NAMES = ("coarse", "detail")
+ST_EMPTY_PALETTE = 8
+
+
+def status_error(status: int, stream: int, pos: int) -> Exception:
+    """The exception the reference raises for one kernel status (codec.py:510-511, :540-543)."""
+    if status == ST_EMPTY_PALETTE:
+        return CorruptStreamError("empty palette")
+    if status in ERROR_TEXT:
+        return CorruptStreamError(f"{ERROR_TEXT[status]} ({STREAM_NAMES[stream]} stream, nibble {pos})")
+    return RuntimeError(f"decoder returned invalid status {status}")
+
+
+def _ptr(a) -> int:
+    """Address of a numpy array / torch tensor / None."""
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _stream_handle(torch, stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class GpuVolume:
+    """One container (or a brick range of it) resident on a CUDA device.
+
+    ``head120`` is the 120-byte CSV1 head, ``directory`` the structured
+    44-byte directory rows of bricks [brick_begin, brick_end), and the blobs
+    are numpy arrays (host upload) or torch CUDA tensors (borrowed, with
+    >=16 readable bytes past their end) starting at the given global bases.
+    """
+
+    def __init__(self, head120: bytes, directory: np.ndarray, palette, coarse, detail,
+                 brick_begin: int = 0, brick_end: int | None = None,
+                 palette_base: int = 0, coarse_base: int = 0, detail_base: int = 0,
+                 device=None, stream=None, on_device: bool = False):
+        torch = _lib.require_cuda()
+        self._torch = torch
+        L = _lib.lib()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   torch.device(device).index or 0)
+        n = directory.shape[0] if not on_device else None
+        if brick_end is None:
+            brick_end = brick_begin + (n if n is not None else directory.numel() // 44)
+        self.brick_begin, self.brick_end = int(brick_begin), int(brick_end)
+        self._keep = (head120, directory, palette, coarse, detail)   # borrowed/host buffers stay alive
+        head = np.frombuffer(bytes(head120[:120]), dtype=np.uint8).copy()
+        self._head = head
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            sh = _stream_handle(torch, stream)
+            if on_device:
+                rc = L.csv_volume_create_device(
+                    self.device.index, _ptr(head), _ptr(directory), self.brick_begin, self.brick_end,
+                    _ptr(palette), palette_base, palette.numel(), _ptr(coarse), coarse_base, coarse.numel(),
+                    _ptr(detail), detail_base, detail.numel(), sh, ctypes.byref(handle))
+            else:
+                d = np.ascontiguousarray(directory).view(np.uint8)
+                pal = np.ascontiguousarray(palette, dtype="<u4")
+                cb = np.ascontiguousarray(coarse, dtype=np.uint8)
+                db = np.ascontiguousarray(detail, dtype=np.uint8) if detail is not None else np.zeros(0, np.uint8)
+                self._keep = (head120, d, pal, cb, db)
+                rc = L.csv_volume_create(
+                    self.device.index, _ptr(head), _ptr(d), self.brick_begin, self.brick_end,
+                    _ptr(pal), palette_base, pal.size, _ptr(cb), coarse_base, cb.size,
+                    _ptr(db), detail_base, db.size, sh, ctypes.byref(handle))
+            _lib.check(rc)
+        self._h = handle
+        dims = (ctypes.c_int64 * 3)()
+        grid = (ctypes.c_int64 * 3)()
+        bl2 = ctypes.c_int()
+        ent = ctypes.c_int()
+        _lib.check(L.csv_volume_info(self._h, dims, grid, ctypes.byref(bl2), ctypes.byref(ent)))
+        self.dims = tuple(dims)          # (x, y, z)
+        self.grid = tuple(grid)
+        self.brick_log2 = bl2.value
+        self.entropy = bool(ent.value)
+
+    # ------------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().csv_volume_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_bricks(self) -> int:
+        return self.brick_end - self.brick_begin
+
+    def crop(self, t: int) -> tuple[int, int, int]:
+        """(z, y, x) extent of the volume at LOD t (container.py:476-478)."""
+        x, y, z = self.dims
+        return tuple(-(-d // (1 << t)) for d in (z, y, x))
+
+    def slab(self, t: int) -> tuple[int, int]:
+        """LOD-t z rows covered by this volume's bricks (whole bz layers assumed)."""
+        gx, gy, _ = self.grid
+        side = (1 << self.brick_log2) >> t
+        z0 = (self.brick_begin // (gx * gy)) * side
+        z1 = min(-(-self.brick_end // (gx * gy)) * side, self.crop(t)[0])
+        return z0, z1
+
+    # ------------------------------------------------------------------ decode
+    def decode(self, t: int = 0, out=None, z_range=None, results=None, stream=None):
+        """Raster decode (K1 + K2/K3) into a (z1-z0, cy, cx) uint32 CUDA tensor."""
+        torch = self._torch
+        if not 0 <= t <= self.brick_log2:
+            raise ValueError(f"LOD {t} outside [0, {self.brick_log2}]")
+        z0, z1 = z_range if z_range is not None else self.slab(t)
+        _, cy, cx = self.crop(t)
+        if out is None:
+            out = torch.empty((max(z1 - z0, 0), cy, cx), dtype=torch.int32, device=self.device)
+        if results is None:
+            results = torch.empty((max(self.n_bricks, 1), 4), dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().csv_decode_volume(self._h, t, _ptr(out), z0, z1, _ptr(results),
+                                                    _stream_handle(torch, stream)))
+        return out, results
+
+    def decode_bricks(self, bricks, lods, dst, pool, results=None, stream=None):
+        """Batched Morton decode (K1 + K2/K4) of (brick, lod) requests into pool[dst:...]."""
+        torch = self._torch
+        n = int(bricks.numel())
+        if results is None:
+            results = torch.empty((max(n, 1), 4), dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().csv_decode_bricks(self._h, n, _ptr(bricks), _ptr(lods), _ptr(dst), _ptr(pool),
+                                                    _ptr(results), _stream_handle(torch, stream)))
+        return results
+
+    def decode_streams(self, bricks, t: int, stream=None):
+        """K1 alone: (entries u8 tensor, offsets [2n+1], per-stream results [2n] structured)."""
+        torch = self._torch
+        L = _lib.lib()
+        n = int(bricks.numel())
+        cap = ctypes.c_uint64()
+        _lib.check(L.csv_streams_capacity(self._h, n, t, ctypes.byref(cap)))
+        entries = torch.zeros(max(int(cap.value), 16), dtype=torch.uint8, device=self.device)
+        offs = torch.zeros(2 * n + 1, dtype=torch.int64, device=self.device)
+        sres = torch.zeros((max(2 * n, 1), 4), dtype=torch.int32, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(L.csv_decode_streams(self._h, n, _ptr(bricks), t, _ptr(entries), entries.numel(),
+                                            _ptr(offs), _ptr(sres), _stream_handle(torch, stream)))
+        return entries, offs, sres
+
+    # ------------------------------------------------------------------ results
+    @staticmethod
+    def results_host(results, n: int) -> np.ndarray:
+        arr = results[:n].contiguous().cpu().numpy()
+        return arr.view(_lib.RESULT_DTYPE).reshape(n)
+
+    @staticmethod
+    def raise_first(results, n: int) -> None:
+        """Raise the reference's exception for the lowest failing index, if any."""
+        if n == 0:
+            return
+        status = results[:n, 0].view(results.dtype)  # low 32 bits hold status (little-endian)
+        st32 = (status & 0xFFFFFFFF)
+        bad = st32.nonzero()
+        if bad.numel() == 0:
+            return
+        i = int(bad[0, 0])
+        row = results[i].cpu().numpy().view(_lib.RESULT_DTYPE)[0]
+        raise status_error(int(row["status"]), int(row["stream"]), int(row["pos"]))
