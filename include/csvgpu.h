@@ -141,6 +141,35 @@ int csv_streams_capacity(csv_volume* vol, uint64_t n, int t, uint64_t* cap);
 /* Volume geometry probe: dims(x,y,z), grid(x,y,z), brick_log2, entropy. */
 int csv_volume_info(csv_volume* vol, int64_t* dims3, int64_t* grid3, int* brick_log2, int* entropy);
 
+/* ---- GPU encoder: replaces compress_volume
+ * (container.py:374-453) with extract_brick/build_pyramid/_encode_kernel/
+ * build_frequency_tables/rans_encode (container.py:352-371, pyramid.py:43-78,
+ * codec.py:126-212, rans.py:73-180).  Output bytes are identical to the
+ * reference's for the same volume and parameters. */
+typedef struct csv_encoded csv_encoded;
+
+/* d_volume: (Z,Y,X) C-order device array of u16 (width 16) or u32 (width 32);
+ * label_width is the header's original-width field (16 or 32). */
+int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, int64_t Y, int64_t Z,
+                      int brick_log2, int64_t prepass_stride, int entropy, int label_width,
+                      uintptr_t stream, csv_encoded** out);
+/* head120 = the CSV1 head; sizes3 = palette entries, coarse bytes, detail bytes. */
+int csv_encoded_info(csv_encoded* enc, uint8_t* head120, uint64_t* n_bricks, uint64_t* sizes3);
+/* Device pointers of the encoded directory rows and blobs (each padded by >= 16 B);
+ * valid until csv_encoded_free.  Suitable for csv_volume_create_device. */
+int csv_encoded_device_ptrs(csv_encoded* enc, const uint8_t** d_dir44, const uint32_t** d_palette,
+                            const uint8_t** d_coarse, const uint8_t** d_detail);
+int csv_encoded_copy_to_host(csv_encoded* enc, uint8_t* dir44, uint32_t* palette, uint8_t* coarse,
+                             uint8_t* detail, uintptr_t stream);
+int csv_encoded_free(csv_encoded* enc);
+
+/* Synthetic jittered-grid Voronoi labels (benchmark configs 2-5):
+ * cells_per_axis^3 seeds, label = nearest seed id + 1; membrane != 0 sets label 0
+ * where the +x/+y/+z neighbour's nearest seed differs; drift (voxels) perturbs
+ * seeds per drift_seed (time series).  d_out: (Z,Y,X) u32. */
+int csv_synth_voronoi(uint32_t* d_out, int64_t X, int64_t Y, int64_t Z, int cells_per_axis, uint32_t seed,
+                      int membrane, double drift, uint32_t drift_seed, uintptr_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@ from .codec import BrickEncoding, decode_brick, decode_brick_entropy, decode_roo
 from .container import (CompressionConfig, CsvContainer, VolumeMeta, decompress_volume,
                         decompress_volume_device)
 from .device import GpuVolume
+from .encode import GpuEncoded, compress_volume, compress_volume_device, synth_voronoi
 from .errors import (CacheCapacityError, ConfigError, CorruptStreamError, CsvolError, EncodabilityError,
                      IngestionError)
 from .morton import BrickConfig, NodeCoord, morton_decode, morton_encode, outside_neighbor
@@ -21,7 +22,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BrickCache", "BrickConfig", "BrickEncoding", "CacheCapacityError", "CacheStats", "CompressionConfig",
     "ConfigError", "CorruptStreamError", "CsvContainer", "CsvolError", "EncodabilityError", "FrequencyTable",
-    "GpuVolume", "IngestionError", "NodeCoord", "TablePair", "VolumeMeta", "build_frequency_tables",
+    "GpuEncoded", "GpuVolume", "compress_volume", "compress_volume_device", "synth_voronoi", "IngestionError", "NodeCoord", "TablePair", "VolumeMeta", "build_frequency_tables",
     "decode_brick", "decode_brick_entropy", "decode_root", "decompress_volume", "decompress_volume_device",
     "iter_operations", "morton_decode", "morton_encode", "outside_neighbor", "quantize_counts",
 ]

@@ -22,6 +22,8 @@ STREAM_RESULT_DTYPE = np.dtype([("n_entries", "<u4"), ("fail_nibble", "<u4"), ("
 EXPORTS = (
     "csv_version", "csv_last_error", "csv_volume_create", "csv_volume_create_device", "csv_volume_free",
     "csv_decode_volume", "csv_decode_bricks", "csv_decode_streams", "csv_streams_capacity", "csv_volume_info",
+    "csv_encode_volume", "csv_encoded_info", "csv_encoded_device_ptrs", "csv_encoded_copy_to_host",
+    "csv_encoded_free", "csv_synth_voronoi",
 )
 
 
@@ -62,6 +64,18 @@ def lib():
         L.csv_streams_capacity.argtypes = [P, U64, I, P]
         L.csv_volume_info.restype = I
         L.csv_volume_info.argtypes = [P, P, P, P, P]
+        L.csv_encode_volume.restype = I
+        L.csv_encode_volume.argtypes = [I, P, I, I64, I64, I64, I, I64, I, I, UP, P]
+        L.csv_encoded_info.restype = I
+        L.csv_encoded_info.argtypes = [P, P, P, P]
+        L.csv_encoded_device_ptrs.restype = I
+        L.csv_encoded_device_ptrs.argtypes = [P, P, P, P, P]
+        L.csv_encoded_copy_to_host.restype = I
+        L.csv_encoded_copy_to_host.argtypes = [P, P, P, P, P, UP]
+        L.csv_encoded_free.restype = I
+        L.csv_encoded_free.argtypes = [P]
+        L.csv_synth_voronoi.restype = I
+        L.csv_synth_voronoi.argtypes = [P, I64, I64, I64, I, ctypes.c_uint32, I, ctypes.c_double, ctypes.c_uint32, UP]
         _lib = L
     return _lib
 

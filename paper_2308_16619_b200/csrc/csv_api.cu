@@ -25,6 +25,7 @@ size_t k2_smem_bytes(int L);
 using namespace csv;
 
 static thread_local std::string g_err;
+namespace csv { void set_error(const char* msg) { g_err = msg; } }
 
 static int fail(int code, const char* fmt, ...) {
     char buf[512];

@@ -338,9 +338,6 @@ __host__ __device__ inline Layout make_layout(int L) {
     Y.words = Y.ipb + maxP;
     return Y;
 }
-__device__ __forceinline__ uint32_t levoff(int j) {   // j = N - level
-    return ((1u << (3 * j)) - 1u) / 7u;
-}
 
 enum { OUT_RASTER = 0, OUT_MORTON = 1 };
 

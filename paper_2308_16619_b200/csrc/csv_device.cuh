@@ -11,6 +11,9 @@
 
 namespace csv {
 
+// thread-local last-error text shared by every C-ABI entry point (csv_last_error)
+void set_error(const char* msg);
+
 constexpr uint32_t kStateLower = 1u << 23;   // rans.py:27
 constexpr int kPrecision = 12;               // rans.py:25
 constexpr uint32_t kTotalFreq = 1u << 12;    // rans.py:26
@@ -101,6 +104,11 @@ __device__ __forceinline__ uint32_t spread3_u32(uint32_t v) {   // 7-bit coordin
     v = (v | (v << 4)) & 0x000C30C3u;
     v = (v | (v << 2)) & 0x00249249u;
     return v;
+}
+
+// offset of level (N - j) inside a coarse-to-fine level array (root first)
+__host__ __device__ __forceinline__ uint32_t levoff(int j) {
+    return ((1u << (3 * j)) - 1u) / 7u;
 }
 
 // ---- SWAR helpers over 8 entry bytes (entry = op | stop<<3 | delta<<4)

@@ -69,9 +69,10 @@ class GpuVolume:
         L = _lib.lib()
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
                                    torch.device(device).index or 0)
-        n = directory.shape[0] if not on_device else None
         if brick_end is None:
-            brick_end = brick_begin + (n if n is not None else directory.numel() // 44)
+            if on_device:
+                raise ValueError("device-resident volumes need an explicit brick_end")
+            brick_end = brick_begin + directory.shape[0]
         self.brick_begin, self.brick_end = int(brick_begin), int(brick_end)
         self._keep = (head120, directory, palette, coarse, detail)   # borrowed/host buffers stay alive
         head = np.frombuffer(bytes(head120[:120]), dtype=np.uint8).copy()
@@ -80,10 +81,16 @@ class GpuVolume:
         with torch.cuda.device(self.device):
             sh = _stream_handle(torch, stream)
             if on_device:
+                # device blobs: either tensors or raw (ptr, count) pairs; borrowed, not copied
+                def pc(x):
+                    return (x[0], x[1]) if isinstance(x, tuple) else (_ptr(x), x.numel())
+                dp, _ = pc(directory) if isinstance(directory, tuple) else (_ptr(directory), 0)
+                pp, pn = pc(palette)
+                cp, cn = pc(coarse)
+                xp, xn = pc(detail)
                 rc = L.csv_volume_create_device(
-                    self.device.index, _ptr(head), _ptr(directory), self.brick_begin, self.brick_end,
-                    _ptr(palette), palette_base, palette.numel(), _ptr(coarse), coarse_base, coarse.numel(),
-                    _ptr(detail), detail_base, detail.numel(), sh, ctypes.byref(handle))
+                    self.device.index, _ptr(head), dp, self.brick_begin, self.brick_end,
+                    pp, palette_base, pn, cp, coarse_base, cn, xp, detail_base, xn, sh, ctypes.byref(handle))
             else:
                 d = np.ascontiguousarray(directory).view(np.uint8)
                 pal = np.ascontiguousarray(palette, dtype="<u4")
