@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 CSV decode path: decoded GVoxel/s, HBM roofline, e2e, CPU baseline.
+
+Workload (BASELINE.json north_star / configs[2]):
+  synthetic 2048^3 jittered-grid Voronoi, ~1M labels (100^3 cells), 1-voxel
+  label-0 membranes, seed 2; brick 32^3, rANS on, prepass stride 512.
+  The volume is generated and encoded on the GPU (byte-identical to the
+  reference encoder, tests/test_gpu_encode.py) before timing.
+
+One step = one full-volume decode at LOD 0 of this rank's brick range (K1
+entropy lanes + K2 replay/raster writer) from HBM-resident compressed data
+into an HBM-resident (Z,Y,X) uint32 output.  Output (34 GB) and input
+(~1.5 GB) both exceed the 126 MB L2, so no flush is needed between steps.
+
+Multi-GPU: whole-bz-layer brick ranges per rank (no data-path collective),
+total work fixed -> "scaling": "strong"; value = all voxels / max-over-ranks time.
+
+`--impl reference` times the reference's CPU algorithm (oracle/ C port, all
+host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "config3": dict(dims=(2048, 2048, 2048), cells=100, seed=2, membrane=True,
+                    desc="config 3: 2048^3 Voronoi, 100^3 cells (~1M labels), 1-voxel label-0 membranes, seed 2"),
+    "config2": dict(dims=(1024, 1024, 1024), cells=22, seed=1, membrane=False,
+                    desc="config 2: 1024^3 cell-like Voronoi, 22^3 cells (~10k labels), seed 1"),
+}
+BRICK_LOG2 = 5
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cache", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------- distributed
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours":
+        torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return world, rank, local
+
+
+def bz_range(gz: int, world: int, rank: int):
+    base, extra = divmod(gz, world)
+    z0 = rank * base + min(rank, extra)
+    return z0, z0 + base + (1 if rank < extra else 0)
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------- CPU baseline (oracle)
+def cpu_baseline(wl, target_s: float = 12.0, layers_cap: int = 8):
+    """Reference CPU decoder (oracle C port, all host threads) on the first bz-layers of the workload."""
+    from oracle import oracle as orc
+    orc.build()
+    cores = len(os.sched_getaffinity(0))
+    X, Y, Z = wl["dims"]
+    b = 1 << BRICK_LOG2
+
+    def make(layers):
+        zs = min(layers * b, Z)
+        # rows [0, zs] (+1 row so membranes of the last row see their +z neighbour)
+        rows = orc.synth_voronoi((X, Y, Z), wl["cells"], wl["seed"], wl["membrane"],
+                                 z_range=(0, min(zs + 1, Z)), threads=cores)[:zs]
+        return orc.compress_volume(np.ascontiguousarray(rows), brick_log2=BRICK_LOG2, threads=cores), zs
+
+    c1, zs = make(1)
+    t0 = time.perf_counter()
+    orc.decompress_volume(c1, 0, threads=cores)
+    one = time.perf_counter() - t0
+    layers = max(1, min(layers_cap, int(target_s / 3 / max(one, 1e-3))))
+    c, zs = make(layers) if layers > 1 else (c1, zs)
+    best = float("inf")
+    for _ in range(3):
+        t0 = time.perf_counter()
+        bad, _, _ = orc.decompress_volume(c, 0, threads=cores)
+        best = min(best, time.perf_counter() - t0)
+        assert bad == -1
+    vox = X * Y * zs
+    return {"value": vox / best / 1e9, "unit": "GVoxel/s", "cores": cores, "kind": "port",
+            "sample": f"first {layers} bz-layer(s) ({X}x{Y}x{zs} = {vox / 1e6:.0f} MVox) of the workload, "
+                      f"oracle-encoded; oracle decompress_volume (C restatement of _decode_kernel + "
+                      f"morton_to_grid placement), {cores} OpenMP threads, best of 3"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    cb = cpu_baseline(wl)
+    X, Y, Z = wl["dims"]
+    line = {"impl": "reference", "metric": "decoded GVoxel/s (full-volume decode, LOD 0)", "value": cb["value"],
+            "unit": "GVoxel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": X * Y * Z / (cb["value"] * 1e9) * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": wl["desc"], "brick": 32, "entropy": "rANS", "lod": 0},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "GVoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- config 4 requests
+def desired_lods(grid, b, cam, fov, height, max_lod):
+    """render.py:145-158 restated: per-brick LOD from brick-centre distance."""
+    gx, gy, gz = grid
+    idx = np.arange(gx * gy * gz)
+    cx = (idx % gx + 0.5) * b
+    cy = (idx // gx % gy + 0.5) * b
+    cz = (idx // (gx * gy) + 0.5) * b
+    d = np.sqrt((cx - cam[0]) ** 2 + (cy - cam[1]) ** 2 + (cz - cam[2]) ** 2)
+    ratio = np.maximum(1.0, d * 2.0 * math.tan(fov / 2.0) / height)
+    lod = np.clip(np.ceil(np.log2(ratio)).astype(np.int64), 0, max_lod)
+    return lod, d
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_2308_16619_b200 as p
+    wl = WORKLOADS[args.workload]
+    X, Y, Z = wl["dims"]
+    dev = torch.device("cuda", local)
+    hbm, peak_kind = peaks()
+    b = 1 << BRICK_LOG2
+    gx, gy, gz = (-(-X // b), -(-Y // b), -(-Z // b))
+    # ---- data: GPU synth + GPU encode (untimed)
+    t0 = time.perf_counter()
+    vol = p.synth_voronoi((X, Y, Z), wl["cells"], wl["seed"], wl["membrane"], device=dev)
+    torch.cuda.synchronize()
+    t_synth = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    enc = p.compress_volume_device(vol, p.CompressionConfig(brick_log2=BRICK_LOG2))
+    torch.cuda.synchronize()
+    t_enc = time.perf_counter() - t0
+    del vol
+    torch.cuda.empty_cache()
+    z0b, z1b = bz_range(gz, world, rank)
+    brick_range = (z0b * gx * gy, z1b * gx * gy)
+    gv = enc.to_volume(brick_range)
+    zr = gv.slab(0)
+    out = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32, device=dev)
+    res = torch.empty((gv.n_bricks, 4), dtype=torch.int64, device=dev)
+    voxels_rank = (zr[1] - zr[0]) * Y * X
+    voxels_all = X * Y * Z
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        gv.decode(0, out=out, results=res)
+    torch.cuda.synchronize()
+    p.GpuVolume.raise_first(res, gv.n_bricks)
+    # ---- timed region
+    clocks = Clocks(local)
+    if not args.profile:
+        clocks.start()
+        time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        gv.decode(0, out=out, results=res)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    clk = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["profile"]}
+    p.GpuVolume.raise_first(res, gv.n_bricks)
+    ms = max_over_ranks(ms_rank, world)
+    value = voxels_all / (ms * 1e-3) / 1e9
+    # ---- per-stage timing (CUDA events on the launching stream, separate pass)
+    gv.set_timing(True)
+    stages = []
+    for _ in range(3):
+        gv.decode(0, out=out, results=res)
+        stages.append(gv.last_timing())
+    gv.set_timing(False)
+    plan_ms, k1_ms, k2_ms = (statistics.median(s[i] for s in stages) for i in range(3))
+    # ---- algorithmic bytes for this rank's bricks
+    cont = enc.to_container() if rank == 0 or world == 1 else enc.to_container()
+    d = cont.directory[brick_range[0]:brick_range[1]]
+    pal_b = 4 * int(d["palette_len"].sum())
+    cb_b = int(d["coarse_bytes"].sum())
+    db_b = int(d["detail_bytes"].sum())
+    n_b = brick_range[1] - brick_range[0]
+    step_bytes = pal_b + cb_b + db_b + 44 * n_b + 64 + 4 * voxels_rank
+    ent, offs, sres = gv.decode_streams(torch.arange(brick_range[0], brick_range[1], dtype=torch.int32,
+                                                     device=dev), 0)
+    entries = int(sres[:, 0].to(torch.int64).sum())
+    k1_bytes = cb_b + db_b + entries + 44 * n_b
+    k2_bytes = entries + pal_b + 44 * n_b + 4 * voxels_rank
+    del ent, offs, sres
+    dom = ("k2_replay", k2_ms, k2_bytes) if k2_ms >= k1_ms else ("k1_streams", k1_ms, k1_bytes)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom[0])
+    except Exception:
+        pass
+    achieved = dom[2] / (dom[1] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes": dom[2], "kernel_ms": dom[1]}
+    step_gbs = step_bytes / (ms_rank * 1e-3) / 1e9
+    line = {
+        "metric": "decoded GVoxel/s (full-volume decode, LOD 0)", "value": value, "unit": "GVoxel/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (GPU Voronoi generator; GPU encoder, byte-identical to the reference encoder)",
+        "config": {"workload": wl["desc"], "brick": 32, "entropy": "rANS", "lod": 0, "bricks": gx * gy * gz,
+                   "compressed_bytes": int(enc.payload_bytes), "compression_rate": enc.payload_bytes / (4 * voxels_all),
+                   "parallelism": f"bz-layer range per rank x{world}",
+                   "l2": "inputs (~%.1f GB compressed) and output (%.1f GB) exceed L2; no flush" %
+                         (enc.payload_bytes / 1e9, 4 * voxels_all / 1e9)},
+        "roofline": roofline,
+        "step_roofline": {"achieved": step_gbs, "peak": hbm, "unit": "GB/s", "frac": step_gbs / hbm,
+                          "algorithmic_bytes": step_bytes, "bytes_per_voxel": step_bytes / voxels_rank},
+        "stages_ms": {"plan": plan_ms, "k1_streams": k1_ms, "k2_replay": k2_ms},
+        "clocks": clk,
+        "gpu_launches": 6 * args.steps,
+        "setup_s": {"synth": t_synth, "encode": t_enc},
+    }
+    # ---- config 4: batched random-access decode into a device brick pool
+    if not args.no_cache and not args.profile and world == 1:
+        lod, dist = desired_lods((gx, gy, gz), b, (1024.0, 1024.0, -64.0), math.pi / 3, 1080, BRICK_LOG2)
+        order = np.argsort(dist, kind="stable")[:65536]
+        reqs = [(int(i), int(lod[i])) for i in order if lod[i] < BRICK_LOG2]
+        cache = p.BrickCache(gx * gy * gz, BRICK_LOG2, pool_bytes=8 << 30, device=dev)
+        cache.begin_frame()
+        for br, l in reqs:
+            cache.mark_used(br, l)
+        placed, live = cache.plan_frame(reqs)
+        arr = np.asarray(live, dtype=np.int64)
+        bricks = torch.from_numpy(arr[:, 0].astype(np.int32)).to(dev)
+        lods = torch.from_numpy(arr[:, 1].astype(np.uint8)).to(dev)
+        dst = torch.from_numpy(arr[:, 2] * 8).to(dev)
+        full = enc.to_volume()
+        cres = torch.empty((len(live), 4), dtype=torch.int64, device=dev)
+        for _ in range(args.warmup):
+            full.decode_bricks(bricks, lods, dst, cache.pool, results=cres)
+        torch.cuda.synchronize()
+        p.GpuVolume.raise_first(cres, len(live))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            full.decode_bricks(bricks, lods, dst, cache.pool, results=cres)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        cms = e0.elapsed_time(e1) / args.steps
+        cvox = int(sum(8 ** (BRICK_LOG2 - int(l)) for l in arr[:, 1]))
+        n0 = int((arr[:, 1] == 0).sum())
+        line["random_brick"] = {"value": cvox / (cms * 1e-3) / 1e9, "unit": "GVoxel/s", "ms_per_step": cms,
+                                "requests": len(live), "lod0": n0, "lod1": len(live) - n0, "voxels": cvox,
+                                "workload": "config 4: camera (1024,1024,-64) +z, H=1080, fov pi/3, "
+                                            "desired_lods, 65,536 nearest bricks -> BrickCache plan -> one "
+                                            "csv_decode_bricks batch into an 8 GiB device pool"}
+        full.close()
+        del cache
+    # ---- e2e: public API, host buffers in, host volume out (pinned)
+    if not args.no_e2e and not args.profile:
+        pin = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32, pin_memory=True)
+        h2d = 0
+        times = []
+        for it in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hv = cont.to_device(device=dev, brick_range=brick_range)
+            dout = p.decompress_volume_device(hv, 0, out=out)
+            pin.copy_(dout, non_blocking=True)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            h2d = (44 * n_b + pal_b + cb_b + db_b)
+            hv.close()
+        e2e_s = max_over_ranks(min(times), world)
+        line["e2e"] = {"value": voxels_all / e2e_s / 1e9, "unit": "GVoxel/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": 4 * voxels_rank + 32 * n_b, "seconds": e2e_s,
+                       "path": "CsvContainer.to_device (H2D of directory+blobs) -> decompress_volume_device -> "
+                               "copy into a pinned host (Z,Y,X) uint32 volume"}
+        del pin
+    if not args.no_cpu and not args.profile and rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline(wl)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

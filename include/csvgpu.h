@@ -141,6 +141,12 @@ int csv_streams_capacity(csv_volume* vol, uint64_t n, int t, uint64_t* cap);
 /* Volume geometry probe: dims(x,y,z), grid(x,y,z), brick_log2, entropy. */
 int csv_volume_info(csv_volume* vol, int64_t* dims3, int64_t* grid3, int* brick_log2, int* entropy);
 
+/* Per-stage device timing of the next decode calls on this volume (CUDA events
+ * recorded on the caller's stream): ms3 = {planning (sizes + scan), K1 entropy
+ * lanes, K2 replay + writer} of the most recent csv_decode_volume/_bricks call. */
+int csv_volume_set_timing(csv_volume* vol, int enable);
+int csv_volume_get_timing(csv_volume* vol, float* ms3);
+
 /* ---- GPU encoder: replaces compress_volume
  * (container.py:374-453) with extract_brick/build_pyramid/_encode_kernel/
  * build_frequency_tables/rans_encode (container.py:352-371, pyramid.py:43-78,

@@ -15,7 +15,7 @@
 namespace csv {
 cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                        unsigned long long* counter, uint32_t* gws, uint64_t gws_stride, int gws_ctas,
-                       int nsm, int min_t, cudaStream_t st);
+                       int nsm, int min_t, cudaStream_t st, cudaEvent_t* ev);
 cudaError_t run_root_raster(const VolView& V, Plan P, cudaStream_t st);
 cudaError_t run_streams_only(const VolView& V, Plan P, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                              unsigned long long* counter, int nsm, cudaStream_t st);
@@ -65,6 +65,8 @@ struct csv_volume {
     uint64_t region_total_t0 = 0;   // sum over bricks of entry regions at t=0 (bytes)
     uint64_t region_max_t0 = 0;     // max over bricks
     int64_t dims[3]{}, grid[3]{};
+    bool timing = false;
+    cudaEvent_t ev[4]{};            // plan start, K1 start, K1 end / K2 start, K2 end
 };
 
 // ---------------------------------------------------------------------------- kernels local to the API
@@ -154,6 +156,7 @@ static void vol_release(csv_volume* v) {
     cudaFree(v->d_soa); cudaFree(v->d_blob); cudaFree(v->d_dtab);
     cudaFree(v->d_sizes); cudaFree(v->d_eoff); cudaFree(v->d_scan); cudaFree(v->d_sres);
     cudaFree(v->d_counter); cudaFree(v->d_entries); cudaFree(v->d_gws);
+    for (auto& e : v->ev) if (e) cudaEventDestroy(e);
     delete v;
 }
 
@@ -351,7 +354,7 @@ int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, 
     P.sres = vol->d_sres;
     P.entries = vol->d_entries;
     CUDA_TRY(run_decode(vol->V, P, 0, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
-                        vol->gws_ctas, vol->nsm, t, st));
+                        vol->gws_ctas, vol->nsm, t, st, vol->timing ? vol->ev : nullptr));
     return CSV_OK;
 }
 
@@ -375,7 +378,7 @@ int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, cons
     P.sres = vol->d_sres;
     P.entries = vol->d_entries;
     CUDA_TRY(run_decode(vol->V, P, 1, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
-                        vol->gws_ctas, vol->nsm, 0, st));
+                        vol->gws_ctas, vol->nsm, 0, st, vol->timing ? vol->ev : nullptr));
     return CSV_OK;
 }
 
@@ -405,6 +408,25 @@ int csv_decode_streams(csv_volume* vol, uint64_t n, const uint32_t* d_brick, int
     P.sres = d_sres;
     P.entries = d_entries;
     CUDA_TRY(run_streams_only(vol->V, P, vol->d_sizes, vol->d_scan, vol->d_counter, vol->nsm, st));
+    return CSV_OK;
+}
+
+int csv_volume_set_timing(csv_volume* vol, int enable) {
+    if (!vol) return fail(CSV_E_ARG, "null volume");
+    CUDA_TRY(cudaSetDevice(vol->device));
+    if (enable && !vol->ev[0])
+        for (auto& e : vol->ev) CUDA_TRY(cudaEventCreate(&e));
+    vol->timing = enable != 0;
+    return CSV_OK;
+}
+
+int csv_volume_get_timing(csv_volume* vol, float* ms3) {
+    if (!vol || !ms3) return fail(CSV_E_ARG, "null argument");
+    if (!vol->timing) return fail(CSV_E_ARG, "timing not enabled");
+    CUDA_TRY(cudaEventSynchronize(vol->ev[3]));
+    CUDA_TRY(cudaEventElapsedTime(&ms3[0], vol->ev[0], vol->ev[1]));
+    CUDA_TRY(cudaEventElapsedTime(&ms3[1], vol->ev[1], vol->ev[2]));
+    CUDA_TRY(cudaEventElapsedTime(&ms3[2], vol->ev[2], vol->ev[3]));
     return CSV_OK;
 }
 

@@ -835,15 +835,18 @@ size_t k2_smem_bytes(int L) { return (size_t)make_layout(L).words * 4; }
 // Decode a plan: sizes -> scan -> K1 -> K2.  Workspace pointers are provided by the caller.
 cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                        unsigned long long* counter, uint32_t* gws, uint64_t gws_stride, int gws_ctas,
-                       int nsm, int min_t, cudaStream_t st) {
+                       int nsm, int min_t, cudaStream_t st, cudaEvent_t* ev) {
     if (P.n == 0) return cudaSuccess;
+    if (ev) cudaEventRecord(ev[0], st);
     unsigned nb = (unsigned)((2 * P.n + 255) / 256);
     k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
     cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    if (ev) cudaEventRecord(ev[1], st);
     if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
     else launch_k1<false>(V, P, counter, nsm, st);
+    if (ev) cudaEventRecord(ev[2], st);
     // K2 smem variant (N - t <= 5)
     int Ls = V.N - min_t;
     if (Ls > 5) Ls = 5;
@@ -863,6 +866,7 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
         if (mode == OUT_RASTER) k2_replay<OUT_RASTER, false><<<g, K2_THREADS, 0, st>>>(V, P, Lg, gws, gws_stride);
         else k2_replay<OUT_MORTON, false><<<g, K2_THREADS, 0, st>>>(V, P, Lg, gws, gws_stride);
     }
+    if (ev) cudaEventRecord(ev[3], st);
     return cudaGetLastError();
 }
 

@@ -185,6 +185,15 @@ class GpuVolume:
                                             _ptr(offs), _ptr(sres), _stream_handle(torch, stream)))
         return entries, offs, sres
 
+    def set_timing(self, enable: bool = True) -> None:
+        _lib.check(_lib.lib().csv_volume_set_timing(self._h, 1 if enable else 0))
+
+    def last_timing(self) -> tuple[float, float, float]:
+        """(plan, K1, K2) milliseconds of the last decode call (CUDA events on its stream)."""
+        ms = (ctypes.c_float * 3)()
+        _lib.check(_lib.lib().csv_volume_get_timing(self._h, ms))
+        return tuple(ms)
+
     # ------------------------------------------------------------------ results
     @staticmethod
     def results_host(results, n: int) -> np.ndarray:

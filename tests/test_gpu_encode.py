@@ -57,3 +57,12 @@ def test_synth_deterministic(pkg):
     b = pkg.synth_voronoi((64, 48, 40), 5, seed=3, membrane=True)
     assert torch.equal(a, b)
     assert int((a == 0).sum()) > 0 and int(a.max()) <= 125
+
+
+@pytest.mark.parametrize("membrane,drift", [(True, 0.0), (False, 0.0), (True, 1.0)])
+def test_synth_matches_oracle(pkg, oracle, membrane, drift):
+    d = pkg.synth_voronoi((70, 50, 33), 6, seed=9, membrane=membrane, drift=drift, drift_seed=4)
+    ref = oracle.synth_voronoi((70, 50, 33), 6, seed=9, membrane=membrane, drift=drift, drift_seed=4)
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), ref)
+    part = oracle.synth_voronoi((70, 50, 33), 6, seed=9, membrane=membrane, drift=drift, drift_seed=4, z_range=(10, 20))
+    assert np.array_equal(part, ref[10:20])
