@@ -56,6 +56,7 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cache", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    ap.add_argument("--zlayers", type=int, default=0, help="profiling: only the first K bz-layers of the volume")
     return ap.parse_args()
 
 
@@ -222,7 +223,10 @@ def desired_lods(grid, b, cam, fov, height, max_lod):
 def run_ours(args, world, rank, local):
     import torch
     import paper_2308_16619_b200 as p
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.zlayers:
+        wl["dims"] = (wl["dims"][0], wl["dims"][1], 32 * args.zlayers)
+        wl["desc"] += f" (first {args.zlayers} bz-layers only)"
     X, Y, Z = wl["dims"]
     dev = torch.device("cuda", local)
     hbm, peak_kind = peaks()

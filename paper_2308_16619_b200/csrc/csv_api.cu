@@ -20,6 +20,7 @@ cudaError_t run_root_raster(const VolView& V, Plan P, cudaStream_t st);
 cudaError_t run_streams_only(const VolView& V, Plan P, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                              unsigned long long* counter, int nsm, cudaStream_t st);
 size_t k2_smem_bytes(int L);
+uint64_t k2_gws_words(int L);
 }  // namespace csv
 
 using namespace csv;
@@ -184,7 +185,7 @@ static int ensure_plan(csv_volume* v, uint64_t n, uint64_t entries_need, int Lg,
         v->entries_cap = cap;
     }
     if (Lg > 5) {
-        uint64_t words = (uint64_t)k2_smem_bytes(Lg) / 4;
+        uint64_t words = k2_gws_words(Lg);
         words = (words + 31) & ~31ull;
         int ctas = v->nsm * 2;
         if (words * ctas > v->gws_words_cap) {

@@ -21,6 +21,7 @@
 //                     brick cache).
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include "csv_device.cuh"
 
 namespace csv {
@@ -318,41 +319,53 @@ __global__ void __launch_bounds__(K1_THREADS) k1_streams(VolView V, Plan P, unsi
 
 // ============================================================================ K2: replay
 // Shared (or global-workspace) layout for one brick, sized for L = N - t levels:
-//   lev  : values of levels t+1..N, Morton order, level k at levoff(N-k)
+//   lev  : values of levels t+1..N in Morton order; level N-j at levoffA(j)
+//          (16-byte aligned for j >= 1 so a parent's 8 children store as 2 x uint4)
 //   mask : 2 x W words, active-parent bitmask ping-pong
-//   wpre : W words, exclusive popcount prefix of the parent mask
-//   ipb  : 8^(L-1) words, i_p at each active parent's first entry (by rank)
+//   wpre : W+1 words, exclusive popcount prefix of the parent mask
+//   ipb  : per active parent (by rank) palette-advance prefix, relative to the level
+//   list : per active parent (by rank) its Morton index -> balanced work split
+// IdxT is u16 in the shared-memory variant (L <= 5: <= 4096 parents, <= 32768
+// entries per level) and u32 in the global-workspace variant (L = 6, 7).
+__host__ __device__ __forceinline__ uint32_t levoffA(int j) {
+    return j == 0 ? 0u : 4u + ((1u << (3 * j)) - 8u) / 7u;
+}
 struct Layout {
-    uint32_t lev, mask, wpre, ipb, words;   // offsets in u32 units
+    uint32_t lev, mask, wpre, ipb, list, words, W;   // offsets in u32 units
 };
-__host__ __device__ inline Layout make_layout(int L) {
+__host__ __device__ inline Layout make_layout(int L, int idx_bytes) {
     Layout Y;
-    uint32_t nlev = 0;
-    for (int j = 0; j < L; ++j) nlev += 1u << (3 * j);
+    uint32_t nlev = levoffA(L);
     uint32_t maxP = 1u << (3 * (L - 1));
-    uint32_t W = (maxP + 31) / 32;
+    Y.W = (maxP + 31) / 32;
     Y.lev = 0;
-    Y.mask = nlev;
-    Y.wpre = Y.mask + 2 * W;
-    Y.ipb = Y.wpre + W + 1;
-    Y.words = Y.ipb + maxP;
+    Y.mask = (nlev + 3) & ~3u;
+    Y.wpre = Y.mask + 2 * Y.W;
+    Y.ipb = (Y.wpre + Y.W + 1 + 3) & ~3u;
+    uint32_t idx_words = (maxP * idx_bytes + 15) / 16 * 4;
+    Y.list = Y.ipb + idx_words;
+    Y.words = Y.list + idx_words;
     return Y;
 }
 
 enum { OUT_RASTER = 0, OUT_MORTON = 1 };
 
-// error key codes (low byte); the key orders by entry index first
-enum { EK_UNDERRUN_NV = 1, EK_BAD_OP = 2, EK_PAL_RANGE = 3, EK_DELTA_RANGE = 4, EK_BAD_NEIGHBOR = 6, EK_LEAF_STOP = 7 };
+// error key = entry << 8 | priority << 4 | status; per entry BAD_OP beats
+// LEAF_STOP beats the op-specific check (codec.py:396-457 order).
+__device__ __forceinline__ unsigned long long ekey(uint32_t ent, int prio, int st) {
+    return ((unsigned long long)ent << 8) | (unsigned)(prio << 4) | (unsigned)st;
+}
+enum { EK_UNDERRUN_NV = 15 };   // status placeholder: entry == K1's n_entries
 
 struct K2Shared {
     unsigned long long errkey;
-    uint32_t red[K2_WARPS + 1];
     uint32_t scan[K2_WARPS + 1];
     uint64_t red64[2][K2_WARPS];
 };
 
-// Block-wide in-place exclusive scan of arr[0..n) (u32), adding `base`; returns total.
-__device__ uint32_t block_scan_inplace(uint32_t* arr, uint32_t n, uint32_t base, K2Shared& S) {
+// Block-wide in-place exclusive scan of arr[0..n); returns the total.
+template <typename T>
+__device__ uint32_t block_scan_inplace(T* arr, uint32_t n, K2Shared& S) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t per = (n + K2_WARPS - 1) / K2_WARPS;
     uint32_t lo = wid * per, hi = min(n, lo + per);
@@ -361,22 +374,25 @@ __device__ uint32_t block_scan_inplace(uint32_t* arr, uint32_t n, uint32_t base,
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane == 0) S.scan[wid] = sum;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int w = 0; w < K2_WARPS; ++w) { uint32_t v = S.scan[w]; S.scan[w] = run; run += v; }
-        S.scan[K2_WARPS] = run;
-    }
-    __syncthreads();
-    uint32_t carry = base + S.scan[wid];
-    for (uint32_t c0 = lo; c0 < hi; c0 += 32) {
-        uint32_t i = c0 + lane;
-        uint32_t v = i < hi ? arr[i] : 0;
-        uint32_t inc = v;
+    if (threadIdx.x < 32) {
+        uint32_t v = lane < K2_WARPS ? S.scan[lane] : 0, inc = v;
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += u;
         }
-        if (i < hi) arr[i] = carry + inc - v;
+        if (lane < K2_WARPS) S.scan[lane] = inc - v;
+        if (lane == K2_WARPS - 1) S.scan[K2_WARPS] = inc;
+    }
+    __syncthreads();
+    uint32_t carry = S.scan[wid];
+    for (uint32_t c0 = lo; c0 < hi; c0 += 32) {
+        uint32_t i = c0 + lane;
+        uint32_t v = i < hi ? (uint32_t)arr[i] : 0, inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (i < hi) arr[i] = (T)(carry + inc - v);
         carry += __shfl_sync(0xffffffffu, inc, 31);
     }
     uint32_t total = S.scan[K2_WARPS];
@@ -395,39 +411,47 @@ __device__ __forceinline__ uint64_t block_sum64(uint64_t v, int slot, K2Shared& 
 }
 
 // Per-level context for child evaluation.
+template <typename IdxT>
 struct LevelCtx {
     const uint32_t* plev;    // parent level values (Morton)
     const uint32_t* pmask;   // parent active bitmask
     const uint32_t* wpre;    // word rank prefix
-    const uint32_t* ipb;     // i_p base per active parent (by rank)
-    const uint64_t* E8;      // entry groups of this stream, group index = entry/8
+    const IdxT* ipb;         // palette-advance prefix per active parent (by rank), level-relative
+    const uint64_t* E8;      // entry groups of this stream
     uint32_t g0;             // first group of this level (e0 / 8)
     uint32_t gcap;           // groups inside the stream's entry region
     const uint32_t* pal;
-    uint32_t plen;
+    int64_t plen;
+    int64_t ipbase;          // i_p before the level's first entry
     int cbits;               // bits per axis at the child level
 };
 
-__device__ __forceinline__ bool is_active(const LevelCtx& C, uint32_t q) {
+template <typename IdxT>
+__device__ __forceinline__ bool is_active(const LevelCtx<IdxT>& C, uint32_t q) {
     return (C.pmask[q >> 5] >> (q & 31)) & 1u;
 }
-__device__ __forceinline__ uint32_t rank_of(const LevelCtx& C, uint32_t q) {
+template <typename IdxT>
+__device__ __forceinline__ uint32_t rank_of(const LevelCtx<IdxT>& C, uint32_t q) {
     return C.wpre[q >> 5] + __popc(C.pmask[q >> 5] & ((1u << (q & 31)) - 1u));
 }
-__device__ __forceinline__ uint64_t load_group(const LevelCtx& C, uint32_t r) {
+template <typename IdxT>
+__device__ __forceinline__ uint64_t load_group(const LevelCtx<IdxT>& C, uint32_t r) {
     uint32_t g = C.g0 + r;
     return g < C.gcap ? __ldg(C.E8 + g) : 0ull;
 }
-__device__ __forceinline__ uint32_t pal_at(const LevelCtx& C, int64_t idx) {
+template <typename IdxT>
+__device__ __forceinline__ uint32_t pal_at(const LevelCtx<IdxT>& C, int64_t idx) {
     idx = idx < 0 ? 0 : idx;
-    idx = idx >= (int64_t)C.plen ? (int64_t)C.plen - 1 : idx;
+    idx = idx >= C.plen ? C.plen - 1 : idx;
     return __ldg(C.pal + idx);
 }
 
-// Value of same-level node nm (already decoded in sequential order, nm < j):
-// inactive parent -> parent's value; otherwise evaluate its entry.  Each
-// even-coordinate hop makes one more coordinate odd, so <= 3 hops.
-__device__ uint32_t neighbor_value(const LevelCtx& C, uint32_t nm) {
+// Value of same-level node nm (decoded earlier in sequential order, nm < j):
+// inactive parent -> the parent's value; otherwise its own entry.  Every
+// even-coordinate hop turns one more coordinate odd, so <= 3 hops
+// (codec.py:402-425 applied transitively).
+template <typename IdxT>
+__device__ __noinline__ uint32_t neighbor_value(const LevelCtx<IdxT>& C, uint32_t nm) {
     for (int hop = 0; hop < 4; ++hop) {
         uint32_t q = nm >> 3;
         int c = nm & 7;
@@ -441,107 +465,99 @@ __device__ uint32_t neighbor_value(const LevelCtx& C, uint32_t nm) {
             int a = op - 1;
             uint32_t M = axis_mask(a, C.cbits);
             uint32_t part = nm & M;
-            if ((c >> a) & 1) {                 // odd: +1 neighbour is decoded later -> its parent
-                if (part == M) return 0;        // outside brick (an earlier error)
-                uint32_t nn = (((part | ~M) + 1u) & M) | (nm & ~M);
-                return C.plev[nn >> 3];
+            if ((c >> a) & 1) {
+                if (part == M) return 0;
+                return C.plev[((((part | ~M) + 1u) & M) | (nm & ~M)) >> 3];
             }
             if (part == 0) return 0;
             nm = ((part - 1u) & M) | (nm & ~M);
             continue;
         }
         if (op == 7) return 0;
-        int64_t ip = (int64_t)C.ipb[r] + prefix_bytes(op_eq(w, 6), c);
-        uint32_t d = e >> 4;
-        int64_t idx = op == 4 ? ip : (op == 5 ? ip - d - 1 : ip + 1);
+        int64_t ip = C.ipbase + (int64_t)C.ipb[r] + prefix_bytes(op_eq(w, 6), c);
+        int64_t idx = op == 4 ? ip : (op == 5 ? ip - (int64_t)(e >> 4) - 1 : ip + 1);
         return pal_at(C, idx);
     }
     return 0;
 }
 
-// Evaluate the 8 children of active parent q whose entries are `w`.
-// Errors are reported as (entry key) via errkey.
-__device__ __forceinline__ void eval_group(const LevelCtx& C, uint32_t q, uint64_t w, uint32_t r,
-                                           uint32_t e_first, uint32_t nvalid, bool leaf,
-                                           uint32_t* v, unsigned long long* errkey) {
-    const uint32_t pv = C.plev[q];
-    const uint64_t pa = op_eq(w, 6);
-    const uint32_t ipq = C.ipb[r];
-    unsigned long long myerr = ~0ull;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        uint32_t e = (uint32_t)(w >> (8 * c)) & 0xFFu;
-        uint32_t op = e & 7u;
-        uint32_t val = pv;
-        int code = 0;
-        if (op >= 1 && op <= 3) {
-            int a = op - 1;
-            uint32_t j = (q << 3) | c;
-            uint32_t M = axis_mask(a, C.cbits);
-            uint32_t part = j & M;
-            if ((c >> a) & 1) {
-                if (part == M) code = EK_BAD_NEIGHBOR;
-                else {
-                    uint32_t nn = (((part | ~M) + 1u) & M) | (j & ~M);
-                    val = C.plev[nn >> 3];
-                }
-            } else {
-                if (part == 0) code = EK_BAD_NEIGHBOR;
-                else val = neighbor_value(C, ((part - 1u) & M) | (j & ~M));
-            }
-        } else if (op >= 4 && op <= 6) {
-            int64_t ip = (int64_t)ipq + prefix_bytes(pa, c);
-            int64_t idx;
-            if (op == 4) idx = ip;
-            else if (op == 5) { idx = ip - (int64_t)(e >> 4) - 1; if (idx < 0) code = EK_DELTA_RANGE; }
-            else { idx = ip + 1; if (idx >= (int64_t)C.plen) code = EK_PAL_RANGE; }
-            val = pal_at(C, idx);
-        } else if (op == 7) {
-            code = EK_BAD_OP;
+// One child of active parent q (entries w, palette-advance base ipq).  Records
+// op-specific errors (priority 2) in myerr when the entry is valid.
+template <typename IdxT>
+__device__ __forceinline__ uint32_t child_value(const LevelCtx<IdxT>& C, uint32_t q, int c, uint64_t w, uint32_t pv,
+                                                int64_t ipq, uint64_t pa, uint32_t ent, uint32_t nvalid,
+                                                unsigned long long& myerr) {
+    const uint32_t e = (uint32_t)(w >> (8 * c)) & 0xFFu;
+    const uint32_t op = e & 7u;
+    if (op == 0 || op == 7) return pv;
+    int st = 0;
+    uint32_t val = pv;
+    if (op <= 3) {
+        const int a = op - 1;
+        const uint32_t j = (q << 3) | c;
+        const uint32_t M = axis_mask(a, C.cbits);
+        const uint32_t part = j & M;
+        if ((c >> a) & 1) {      // odd: the +1 neighbour is decoded later -> its parent's value
+            if (part == M) st = CSV_ST_BAD_NEIGHBOR;
+            else val = C.plev[((((part | ~M) + 1u) & M) | (j & ~M)) >> 3];
+        } else {                 // even: the -1 neighbour, same level
+            if (part == 0) st = CSV_ST_BAD_NEIGHBOR;
+            else val = neighbor_value(C, ((part - 1u) & M) | (j & ~M));
         }
-        if (op != 7 && leaf && (e & 8u)) code = EK_LEAF_STOP;   // checked before the op (codec.py:396-399)
-        v[c] = val;
-        uint32_t ent = e_first + c;
-        if (code && ent < nvalid) {
-            unsigned long long key = ((unsigned long long)ent << 8) | (unsigned)code;
-            myerr = key < myerr ? key : myerr;
-        }
-    }
-    if (myerr != ~0ull) atomicMin(errkey, myerr);
-}
-
-// Final-level writer, raster (Z,Y,X) slab: children of parent (qx,qy,qz).
-__device__ __forceinline__ void store_raster(const Plan& P, int64_t ox, int64_t oy, int64_t oz,
-                                             const uint32_t* v) {
-#pragma unroll
-    for (int dz = 0; dz < 2; ++dz) {
-        int64_t z = oz + dz;
-        if (z < P.z_begin || z >= P.z_end) continue;
-#pragma unroll
-        for (int dy = 0; dy < 2; ++dy) {
-            int64_t y = oy + dy;
-            if (y >= P.cy) continue;
-            uint32_t* row = P.out + ((z - P.z_begin) * P.cy + y) * P.cx;
-            uint32_t a = v[dz * 4 + dy * 2], b = v[dz * 4 + dy * 2 + 1];
-            if (ox + 1 < P.cx) {
-                uint32_t* p = row + ox;
-                if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
-                else { p[0] = a; p[1] = b; }
-            } else if (ox < P.cx) {
-                row[ox] = a;
-            }
-        }
-    }
-}
-
-__device__ __forceinline__ void store_morton(uint32_t* out, uint32_t q, const uint32_t* v, bool al16) {
-    uint32_t* p = out + 8ull * q;
-    if (al16) {
-        reinterpret_cast<uint4*>(p)[0] = make_uint4(v[0], v[1], v[2], v[3]);
-        reinterpret_cast<uint4*>(p)[1] = make_uint4(v[4], v[5], v[6], v[7]);
     } else {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) p[c] = v[c];
+        const int64_t ip = ipq + prefix_bytes(pa, c);
+        int64_t idx;
+        if (op == 4) idx = ip;
+        else if (op == 5) { idx = ip - (int64_t)(e >> 4) - 1; if (idx < 0) st = CSV_ST_DELTA_RANGE; }
+        else { idx = ip + 1; if (idx >= C.plen) st = CSV_ST_PALETTE_RANGE; }
+        val = pal_at(C, idx);
+    }
+    if (st && ent < nvalid) {
+        unsigned long long k = ekey(ent, 2, st);
+        myerr = k < myerr ? k : myerr;
+    }
+    return val;
+}
+
+// BAD_OP / LEAF_STOP of a whole group at once (SWAR over the 8 entry bytes).
+__device__ __forceinline__ unsigned long long group_flag_errors(uint64_t w, uint32_t e_first, uint32_t nvalid, bool leaf) {
+    const uint64_t ones = 0x0101010101010101ull;
+    uint64_t valid = e_first >= nvalid ? 0ull : (nvalid - e_first >= 8 ? ~0ull : ((1ull << (8 * (nvalid - e_first))) - 1ull));
+    uint64_t b7 = op_eq(w, 7) & valid;
+    uint64_t st = leaf ? (((w >> 3) & ones) & valid & ~b7) : 0ull;
+    if (!(b7 | st)) return ~0ull;
+    unsigned long long k = ~0ull;
+    if (b7) k = ekey(e_first + (__ffsll((long long)b7) - 1) / 8, 0, CSV_ST_BAD_OP);
+    if (st) {
+        unsigned long long k2 = ekey(e_first + (__ffsll((long long)st) - 1) / 8, 1, CSV_ST_LEAF_STOP);
+        k = k2 < k ? k2 : k;
+    }
+    return k;
+}
+
+struct RasterCtx {
+    uint32_t* base;     // voxel (bx*side, by*side, bz*side) of the slab, may be out of slab
+    int64_t ox, oy, oz; // brick origin (LOD-t voxels)
+    int64_t cx, cy;     // row pitch / plane
+    int64_t zb, ze;
+    bool fast;          // brick fully inside crop and slab, 8-byte aligned rows
+};
+
+__device__ __forceinline__ void store_pair(const RasterCtx& R, const Plan& P, int64_t x, int64_t y, int64_t z,
+                                           uint32_t a, uint32_t b) {
+    if (R.fast) {
+        uint32_t* p = R.base + (z * R.cy + y) * R.cx + x;
+        *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
+        return;
+    }
+    int64_t gz = R.oz + z, gy = R.oy + y, gx = R.ox + x;
+    if (gz < R.zb || gz >= R.ze || gy >= R.cy || gx >= R.cx) return;
+    uint32_t* p = P.out + ((gz - R.zb) * R.cy + gy) * R.cx + gx;
+    if (gx + 1 < R.cx) {
+        if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
+        else { p[0] = a; p[1] = b; }
+    } else {
+        p[0] = a;
     }
 }
 
@@ -556,48 +572,64 @@ __device__ __forceinline__ void write_result(const Plan& P, uint64_t r, int st, 
 
 // Fill the whole output of request r with one value (relevant == 0, codec.py:353-358).
 template <int MODE>
-__device__ void fill_output(const VolView& V, const Plan& P, uint64_t b, int t, uint32_t* out_m, uint32_t val) {
-    int side = 1 << (V.N - t);
+__device__ void fill_output(const VolView& V, const Plan& P, const RasterCtx& R, int t, uint32_t* out_m, uint32_t val) {
+    const int lb = V.N - t;
+    const uint64_t n = 1ull << (3 * lb);
     if (MODE == OUT_MORTON) {
-        uint64_t n = 1ull << (3 * (V.N - t));
         for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) out_m[i] = val;
     } else {
-        int64_t bx = (int64_t)((V.brick_begin + b) % V.gx), by = (int64_t)(((V.brick_begin + b) / V.gx) % V.gy),
-                bz = (int64_t)((V.brick_begin + b) / (V.gx * V.gy));
-        uint64_t n = 1ull << (3 * (V.N - t));
-        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-            int64_t x = i & (side - 1), y = (i >> (V.N - t)) & (side - 1), z = i >> (2 * (V.N - t));
-            int64_t gx = bx * side + x, gy = by * side + y, gz = bz * side + z;
-            if (gx < P.cx && gy < P.cy && gz >= P.z_begin && gz < P.z_end)
-                P.out[((gz - P.z_begin) * P.cy + gy) * P.cx + gx] = val;
+        const int side = 1 << lb;
+        for (uint64_t i = threadIdx.x; i < n / 2; i += blockDim.x) {
+            int64_t x = (2 * i) & (side - 1), y = ((2 * i) >> lb) & (side - 1), z = (2 * i) >> (2 * lb);
+            if (side == 1) { x = 0; y = 0; z = 0; }
+            store_pair(R, P, x, y, z, val, val);
+        }
+        if (side == 1 && threadIdx.x == 0) {
+            if (R.oz >= R.zb && R.oz < R.ze && R.oy < R.cy && R.ox < R.cx)
+                P.out[((R.oz - R.zb) * R.cy + R.oy) * R.cx + R.ox] = val;
         }
     }
 }
 
 template <int MODE, bool SMEM>
-__global__ void __launch_bounds__(K2_THREADS) k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
+__global__ void __launch_bounds__(K2_THREADS, SMEM ? 5 : 1)
+k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
+    using IdxT = typename std::conditional<SMEM, uint16_t, uint32_t>::type;
     extern __shared__ __align__(16) uint32_t dsm[];
     __shared__ K2Shared S;
-    const Layout Y = make_layout(Lmax);
+    const Layout Y = make_layout(Lmax, sizeof(IdxT));
     uint32_t* ws = SMEM ? dsm : gws + blockIdx.x * ws_stride;
+    uint32_t* lev = ws + Y.lev;
+    uint32_t* mask0 = ws + Y.mask;
+    uint32_t* wpre = ws + Y.wpre;
+    IdxT* ipb = reinterpret_cast<IdxT*>(ws + Y.ipb);
+    IdxT* list = reinterpret_cast<IdxT*>(ws + Y.list);
+    const int N = V.N;
     for (uint64_t r = blockIdx.x; r < P.n; r += gridDim.x) {
         const uint64_t b = req_local(V, P, r);
         const int t = req_lod(P, r);
-        const int N = V.N;
         if (b >= V.nb || t > N) { write_result(P, r, -1, 0, 0, 0, 0); continue; }
-        // this variant handles N - t <= Lmax; others belong to the other launch
-        if (t < N && N - t > Lmax) continue;
+        if (t < N && N - t > Lmax) continue;           // belongs to the other variant
         if (!SMEM && N - t <= 5) continue;
         uint32_t* out_m = MODE == OUT_MORTON ? P.out + P.dst[r] : nullptr;
         const uint32_t plen = V.pal_len[b];
         const uint32_t* pal = V.palette + V.pal_off[b];
+        RasterCtx R{};
+        if (MODE == OUT_RASTER) {
+            const uint64_t gb = V.brick_begin + b;
+            const int64_t side = 1ll << (N - t);
+            R.ox = (int64_t)(gb % V.gx) * side;
+            R.oy = (int64_t)((gb / V.gx) % V.gy) * side;
+            R.oz = (int64_t)(gb / (V.gx * V.gy)) * side;
+            R.cx = P.cx; R.cy = P.cy; R.zb = P.z_begin; R.ze = P.z_end;
+            R.base = P.out + ((R.oz - R.zb) * R.cy + R.oy) * R.cx + R.ox;
+            R.fast = side >= 2 && R.ox + side <= R.cx && R.oy + side <= R.cy && R.oz >= R.zb && R.oz + side <= R.ze &&
+                     (R.cx & 1) == 0 && ((reinterpret_cast<uintptr_t>(P.out) & 7) == 0);
+        }
         if (plen == 0) { write_result(P, r, CSV_ST_EMPTY_PALETTE, 0, 0, 0, 0); continue; }
         if (t == N) {   // coarsest LOD: palette[0] (codec.py:514-516, container.py:178-182)
-            if (threadIdx.x == 0) {
-                uint32_t v0 = __ldg(pal);
-                if (MODE == OUT_MORTON) out_m[0] = v0;
-                else fill_output<MODE>(V, P, b, t, nullptr, v0);
-            }
+            if (MODE == OUT_MORTON) { if (threadIdx.x == 0) out_m[0] = __ldg(pal); }
+            else fill_output<MODE>(V, P, R, t, nullptr, __ldg(pal));
             write_result(P, r, 0, 0, 0, 0, 0);
             continue;
         }
@@ -608,44 +640,33 @@ __global__ void __launch_bounds__(K2_THREADS) k2_replay(VolView V, Plan P, int L
             if (t == 0 && nd_raw > 0 && V.d_bytes[b] < 4) { write_result(P, r, CSV_ST_UNDERRUN, 1, 0, 0, 0); continue; }
         }
         if ((uint64_t)nc + nd == 0) {
-            fill_output<MODE>(V, P, b, t, out_m, __ldg(pal));
+            fill_output<MODE>(V, P, R, t, out_m, __ldg(pal));
             write_result(P, r, 0, 0, 0, 0, 0);
             continue;
         }
-        const csv_stream_result sr[2] = {P.sres[2 * r], P.sres[2 * r + 1]};
-        const uint64_t* E8[2] = {reinterpret_cast<const uint64_t*>(P.entries + P.eoff[2 * r]),
-                                 reinterpret_cast<const uint64_t*>(P.entries + P.eoff[2 * r + 1])};
-        const uint32_t gcap[2] = {(uint32_t)((P.eoff[2 * r + 1] - P.eoff[2 * r]) >> 3),
-                                  (uint32_t)((P.eoff[2 * r + 2] - P.eoff[2 * r + 1]) >> 3)};
-        uint32_t* lev = ws + Y.lev;
-        uint32_t* mask0 = ws + Y.mask;
-        const uint32_t Wmax = (Y.wpre - Y.mask) / 2;
-        uint32_t* wpre = ws + Y.wpre;
-        uint32_t* ipb = ws + Y.ipb;
+        const csv_stream_result src = P.sres[2 * r], srd = P.sres[2 * r + 1];
+        const uint64_t eo0 = P.eoff[2 * r], eo1 = P.eoff[2 * r + 1], eo2 = P.eoff[2 * r + 2];
+        const Layout& Yl = Y;
         if (threadIdx.x == 0) {
             lev[0] = __ldg(pal);      // root (codec.py:353)
             mask0[0] = 1u;
             S.errkey = ~0ull;
         }
         __syncthreads();
-        uint32_t cursor[2] = {0, 0};
-        uint64_t pd_acc[2] = {0, 0};
-        uint32_t ipbase = 0;
+        uint32_t cur_c = 0, cur_d = 0;
+        uint64_t pd_c = 0, pd_d = 0;
+        int64_t ipbase = 0;
         int cur = 0;
         bool failed = false;
-        int64_t bx = 0, by = 0, bz = 0;
-        if (MODE == OUT_RASTER) {
-            uint64_t gb = V.brick_begin + b;
-            bx = (int64_t)(gb % V.gx); by = (int64_t)((gb / V.gx) % V.gy); bz = (int64_t)(gb / (V.gx * V.gy));
-        }
         for (int l = N; l > t; --l) {
-            const int s = l == 1 ? 1 : 0;
             const bool leaf = l == 1;
             const bool final_level = (l - 1 == t);
             const uint32_t Pn = 1u << (3 * (N - l));
             const uint32_t W = (Pn + 31) >> 5;
-            uint32_t* pmask = mask0 + cur * Wmax;
-            uint32_t* cmask = mask0 + (cur ^ 1) * Wmax;
+            uint32_t* pmask = mask0 + cur * Yl.W;
+            uint32_t* cmask = mask0 + (cur ^ 1) * Yl.W;
+            const csv_stream_result& sr = leaf ? srd : src;
+            const uint32_t e0 = leaf ? cur_d : cur_c;
             // (A) rank prefix of active parents
             for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
                 uint32_t mw = pmask[i];
@@ -654,127 +675,160 @@ __global__ void __launch_bounds__(K2_THREADS) k2_replay(VolView V, Plan P, int L
                 wpre[i] = __popc(mw);
             }
             __syncthreads();
-            const uint32_t nact = block_scan_inplace(wpre, W, 0, S);
-            // (B) palette-advance counts per active parent, scanned into i_p bases
-            LevelCtx C;
-            C.plev = lev + levoff(N - l);
+            const uint32_t nact = block_scan_inplace(wpre, W, S);
+            LevelCtx<IdxT> C;
+            C.plev = lev + levoffA(N - l);
             C.pmask = pmask;
             C.wpre = wpre;
             C.ipb = ipb;
-            C.E8 = E8[s];
-            C.g0 = cursor[s] >> 3;
-            C.gcap = gcap[s];
+            C.E8 = reinterpret_cast<const uint64_t*>(P.entries + (leaf ? eo1 : eo0));
+            C.g0 = e0 >> 3;
+            C.gcap = (uint32_t)(((leaf ? eo2 : eo1) - (leaf ? eo1 : eo0)) >> 3);
             C.pal = pal;
             C.plen = plen;
+            C.ipbase = ipbase;
             C.cbits = N - l + 1;
+            // (B) active list + palette-advance counts per active parent
+            for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
+                uint32_t mw = pmask[i], rk = wpre[i];
+                while (mw) {
+                    int bit = __ffs(mw) - 1;
+                    mw &= mw - 1;
+                    list[rk++] = (IdxT)(32 * i + bit);
+                }
+            }
             uint64_t pdl = 0;
             for (uint32_t i = threadIdx.x; i < nact; i += blockDim.x) {
                 uint64_t w = load_group(C, i);
-                ipb[i] = __popcll(op_eq(w, 6));
+                ipb[i] = (IdxT)__popcll(op_eq(w, 6));
                 pdl += __popcll(op_eq(w, 5));
             }
-            pd_acc[s] += pdl;
+            if (leaf) pd_d += pdl; else pd_c += pdl;
             __syncthreads();
-            const uint32_t tot_pa = block_scan_inplace(ipb, nact, ipbase, S);
-            const uint32_t nvalid = sr[s].n_entries;
-            const uint32_t e0 = cursor[s];
-            // (C) evaluate children
-            uint32_t* clev = final_level ? nullptr : lev + levoff(N - l + 1);
-            if (final_level && MODE == OUT_RASTER) {
-                const int pb = N - l;   // bits per axis at the parent level
-                const int64_t side_t = 1ll << (N - t);
-                for (uint32_t i = threadIdx.x; i < Pn; i += blockDim.x) {
-                    uint32_t qx = i & ((1u << pb) - 1u), qy = (i >> pb) & ((1u << pb) - 1u), qz = i >> (2 * pb);
-                    uint32_t q = spread3_u32(qx) | (spread3_u32(qy) << 1) | (spread3_u32(qz) << 2);
-                    uint32_t v[8];
-                    if (is_active(C, q)) {
-                        uint32_t rk = rank_of(C, q);
-                        uint64_t w = load_group(C, rk);
-                        eval_group(C, q, w, rk, e0 + 8 * rk, nvalid, leaf, v, &S.errkey);
-                    } else {
-                        uint32_t pv = C.plev[q];
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) v[c] = pv;
+            const uint32_t tot_pa = block_scan_inplace(ipb, nact, S);
+            const uint32_t nvalid = sr.n_entries;
+            // (C1) active parents, balanced by rank
+            unsigned long long myerr = ~0ull;
+            uint32_t* clev = final_level ? nullptr : lev + levoffA(N - l + 1);
+            for (uint32_t rk = threadIdx.x; rk < nact; rk += blockDim.x) {
+                const uint32_t q = list[rk];
+                const uint64_t w = load_group(C, rk);
+                const uint32_t ent0 = e0 + 8 * rk;
+                const uint32_t pv = C.plev[q];
+                const int64_t ipq = ipbase + (int64_t)ipb[rk];
+                const uint64_t pa = op_eq(w, 6);
+                unsigned long long fe = group_flag_errors(w, ent0, nvalid, leaf);
+                myerr = fe < myerr ? fe : myerr;
+                if (final_level && MODE == OUT_RASTER) {
+                    const int pb = N - l;
+                    const int64_t x0 = 2 * (int64_t)compact3(q), y0 = 2 * (int64_t)compact3(q >> 1),
+                                  z0 = 2 * (int64_t)compact3(q >> 2);
+                    (void)pb;
+#pragma unroll 1
+                    for (int row = 0; row < 4; ++row) {
+                        const int c0 = 2 * row;
+                        uint32_t a = child_value(C, q, c0, w, pv, ipq, pa, ent0 + c0, nvalid, myerr);
+                        uint32_t bb = child_value(C, q, c0 + 1, w, pv, ipq, pa, ent0 + c0 + 1, nvalid, myerr);
+                        store_pair(R, P, x0, y0 + (row & 1), z0 + (row >> 1), a, bb);
                     }
-                    store_raster(P, bx * side_t + 2 * qx, by * side_t + 2 * qy, bz * side_t + 2 * qz, v);
+                } else {
+                    uint32_t v[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) v[c] = child_value(C, q, c, w, pv, ipq, pa, ent0 + c, nvalid, myerr);
+                    uint32_t* dstp = final_level ? out_m + 8ull * q : clev + 8 * q;
+                    if (!final_level || ((reinterpret_cast<uintptr_t>(dstp) & 15) == 0)) {
+                        reinterpret_cast<uint4*>(dstp)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                        reinterpret_cast<uint4*>(dstp)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) dstp[c] = v[c];
+                    }
+                    if (!final_level) {
+                        // stop bits -> inactive children (codec.py:460-463), packed to one byte
+                        uint64_t st = (w >> 3) & 0x0101010101010101ull;
+                        reinterpret_cast<uint8_t*>(cmask)[q] = (uint8_t)(~(uint32_t)((st * 0x0102040810204080ull) >> 56));
+                    }
+                }
+            }
+            if (myerr != ~0ull) atomicMin(&S.errkey, myerr);
+            // (C2) inactive parents: their children repeat the parent value
+            if (final_level && MODE == OUT_RASTER) {
+                const int pb = N - l;
+                const uint32_t pm = (1u << pb) - 1u;
+                for (uint32_t i = threadIdx.x; i < Pn; i += blockDim.x) {
+                    const uint32_t qx = i & pm, qy = (i >> pb) & pm, qz = i >> (2 * pb);
+                    const uint32_t q = spread3_u32(qx) | (spread3_u32(qy) << 1) | (spread3_u32(qz) << 2);
+                    if (is_active(C, q)) continue;
+                    const uint32_t pv = C.plev[q];
+#pragma unroll
+                    for (int row = 0; row < 4; ++row)
+                        store_pair(R, P, 2 * qx, 2 * qy + (row & 1), 2 * qz + (row >> 1), pv, pv);
                 }
             } else {
-                const bool al16 = MODE == OUT_MORTON && ((reinterpret_cast<uintptr_t>(out_m) & 15) == 0);
                 for (uint32_t q = threadIdx.x; q < Pn; q += blockDim.x) {
-                    uint32_t v[8];
-                    uint32_t cm = 0;
-                    if (is_active(C, q)) {
-                        uint32_t rk = rank_of(C, q);
-                        uint64_t w = load_group(C, rk);
-                        eval_group(C, q, w, rk, e0 + 8 * rk, nvalid, leaf, v, &S.errkey);
-                        // stop bits -> inactive children (codec.py:460-463); packed to one byte
-                        uint64_t st = (w >> 3) & 0x0101010101010101ull;
-                        cm = (~(uint32_t)((st * 0x0102040810204080ull) >> 56)) & 0xFFu;
-                    } else {
-                        uint32_t pv = C.plev[q];
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) v[c] = pv;
-                    }
-                    if (final_level) {
-                        store_morton(out_m, q, v, al16);
+                    if (is_active(C, q)) continue;
+                    const uint32_t pv = C.plev[q];
+                    uint32_t* dstp = final_level ? out_m + 8ull * q : clev + 8 * q;
+                    if (!final_level || ((reinterpret_cast<uintptr_t>(dstp) & 15) == 0)) {
+                        reinterpret_cast<uint4*>(dstp)[0] = make_uint4(pv, pv, pv, pv);
+                        reinterpret_cast<uint4*>(dstp)[1] = make_uint4(pv, pv, pv, pv);
                     } else {
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) clev[8 * q + c] = v[c];
-                        reinterpret_cast<uint8_t*>(cmask)[q] = (uint8_t)cm;
+                        for (int c = 0; c < 8; ++c) dstp[c] = pv;
                     }
+                    if (!final_level) reinterpret_cast<uint8_t*>(cmask)[q] = 0;
                 }
             }
-            if (threadIdx.x == 0 && (uint64_t)e0 + 8ull * nact > nvalid) {
-                unsigned long long key = ((unsigned long long)nvalid << 8) | EK_UNDERRUN_NV;
-                atomicMin(&S.errkey, key);
-            }
+            if (threadIdx.x == 0 && (uint64_t)e0 + 8ull * nact > nvalid)
+                atomicMin(&S.errkey, ekey(nvalid, 0, EK_UNDERRUN_NV));
             __syncthreads();
             const unsigned long long ek = S.errkey;
             if (ek != ~0ull) {
                 // first failing entry in sequential order -> status + nibble position
                 const uint32_t ent = (uint32_t)(ek >> 8);
-                const int code = (int)(ek & 0xFF);
+                const int code = (int)(ek & 0xF);
                 int st;
                 int64_t pos;
                 if (code == EK_UNDERRUN_NV) {
-                    const csv_stream_result& q = sr[s];
-                    if ((q.flags & CSV_SF_PARTIAL) && leaf && (q.partial_op & 8u)) {
+                    if ((sr.flags & CSV_SF_PARTIAL) && leaf && (sr.partial_op & 8u)) {
                         st = CSV_ST_LEAF_STOP;
-                        pos = (int64_t)q.fail_nibble - 1;
+                        pos = (int64_t)sr.fail_nibble - 1;
                     } else {
                         st = CSV_ST_UNDERRUN;
-                        pos = (q.flags & CSV_SF_FAILED) ? (int64_t)q.fail_nibble : (int64_t)ent;
+                        pos = (sr.flags & CSV_SF_FAILED) ? (int64_t)sr.fail_nibble : (int64_t)ent;
                     }
                 } else {
                     // nibble index of entry `ent` = ent + #payload nibbles before it
+                    const uint64_t* E8 = C.E8;
                     uint64_t cnt = 0;
                     for (uint32_t g = threadIdx.x; g < (ent + 7) / 8; g += blockDim.x) {
-                        uint64_t w = (g < gcap[s]) ? __ldg(E8[s] + g) : 0ull;
+                        uint64_t w = (g < C.gcap) ? __ldg(E8 + g) : 0ull;
                         uint32_t lim = ent - 8 * g;
-                        if (lim < 8) w &= (1ull << (8 * lim)) - 1ull;
-                        cnt += __popcll(op_eq(w, 5) & ((lim < 8) ? ((1ull << (8 * lim)) - 1ull) : ~0ull));
+                        uint64_t m = op_eq(w, 5);
+                        if (lim < 8) m &= (1ull << (8 * lim)) - 1ull;
+                        cnt += __popcll(m);
                     }
                     pos = (int64_t)ent + (int64_t)block_sum64(cnt, 0, S);
                     st = code;
-                    if (code == EK_DELTA_RANGE) pos += 1;   // reported at the payload nibble
+                    if (code == CSV_ST_DELTA_RANGE) pos += 1;   // reported at the payload nibble
                 }
-                write_result(P, r, st, s, pos, 0, 0);
+                write_result(P, r, st, leaf ? 1 : 0, pos, 0, 0);
                 failed = true;
                 break;
             }
-            cursor[s] = e0 + 8 * nact;
+            if (leaf) cur_d = e0 + 8 * nact; else cur_c = e0 + 8 * nact;
             ipbase += tot_pa;
             cur ^= 1;
         }
         if (!failed) {
-            const int64_t pdc = (int64_t)block_sum64(pd_acc[0], 0, S);
-            const int64_t pdd = (int64_t)block_sum64(pd_acc[1], 1, S);
-            const int64_t ci = (int64_t)cursor[0] + pdc, di = (int64_t)cursor[1] + pdd;
+            const int64_t pdc = (int64_t)block_sum64(pd_c, 0, S);
+            const int64_t pdd = (int64_t)block_sum64(pd_d, 1, S);
+            const int64_t ci = (int64_t)cur_c + pdc, di = (int64_t)cur_d + pdd;
             int st = 0, stream = 0;
             int64_t pos = 0;
             if (V.entropy) {   // full consumption must land on the initial state (codec.py:464-470)
-                if (nc_raw > 0 && ci == (int64_t)nc_raw && (sr[0].flags & CSV_SF_DESYNC)) { st = CSV_ST_DESYNC; stream = 0; pos = ci; }
-                else if (t == 0 && nd_raw > 0 && di == (int64_t)nd_raw && (sr[1].flags & CSV_SF_DESYNC)) { st = CSV_ST_DESYNC; stream = 1; pos = di; }
+                if (nc_raw > 0 && ci == (int64_t)nc_raw && (src.flags & CSV_SF_DESYNC)) { st = CSV_ST_DESYNC; stream = 0; pos = ci; }
+                else if (t == 0 && nd_raw > 0 && di == (int64_t)nd_raw && (srd.flags & CSV_SF_DESYNC)) { st = CSV_ST_DESYNC; stream = 1; pos = di; }
             }
             write_result(P, r, st, stream, pos, ci, di);
         }
@@ -830,7 +884,8 @@ cudaError_t run_scan(const uint64_t* sizes, uint64_t* out, uint64_t n, uint64_t*
     return cudaGetLastError();
 }
 
-size_t k2_smem_bytes(int L) { return (size_t)make_layout(L).words * 4; }
+size_t k2_smem_bytes(int L) { return (size_t)make_layout(L, 2).words * 4; }
+uint64_t k2_gws_words(int L) { return make_layout(L, 4).words; }
 
 // Decode a plan: sizes -> scan -> K1 -> K2.  Workspace pointers are provided by the caller.
 cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, uint64_t* scan_tmp,

@@ -111,6 +111,14 @@ __host__ __device__ __forceinline__ uint32_t levoff(int j) {
     return ((1u << (3 * j)) - 1u) / 7u;
 }
 
+__device__ __forceinline__ uint32_t compact3(uint32_t v) {   // bits 0,3,6.. -> 0,1,2..
+    v &= 0x00249249u;
+    v = (v ^ (v >> 2)) & 0x000C30C3u;
+    v = (v ^ (v >> 4)) & 0x0000F00Fu;
+    v = (v ^ (v >> 8)) & 0x000000FFu;
+    return v;
+}
+
 // ---- SWAR helpers over 8 entry bytes (entry = op | stop<<3 | delta<<4)
 __device__ __forceinline__ uint64_t op_eq(uint64_t w, uint32_t op) {
     const uint64_t ones = 0x0101010101010101ull;

@@ -51,13 +51,6 @@ __device__ __forceinline__ uint64_t enc_brick(const EncView& E, uint64_t i) {
     return E.list ? (uint64_t)E.list[i] : E.b0 + i;
 }
 
-__device__ __forceinline__ uint32_t compact3(uint32_t v) {   // bits 0,3,6.. -> 0,1,2..
-    v &= 0x00249249u;
-    v = (v ^ (v >> 2)) & 0x000C30C3u;
-    v = (v ^ (v >> 4)) & 0x0000F00Fu;
-    v = (v ^ (v >> 8)) & 0x000000FFu;
-    return v;
-}
 
 __device__ __forceinline__ uint32_t voxel(const EncView& E, int64_t x, int64_t y, int64_t z) {
     x = x < E.X ? x : E.X - 1;
