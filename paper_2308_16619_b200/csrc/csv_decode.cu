@@ -320,18 +320,19 @@ __global__ void __launch_bounds__(K1_THREADS) k1_streams(VolView V, Plan P, unsi
 // ============================================================================ K2: replay
 // Shared (or global-workspace) layout for one brick, sized for L = N - t levels:
 //   lev  : values of levels t+1..N in Morton order; level N-j at levoffA(j)
-//          (16-byte aligned for j >= 1 so a parent's 8 children store as 2 x uint4)
+//          (16-byte aligned for j >= 1)
 //   mask : 2 x W words, active-parent bitmask ping-pong
 //   wpre : W+1 words, exclusive popcount prefix of the parent mask
-//   ipb  : per active parent (by rank) palette-advance prefix, relative to the level
-//   list : per active parent (by rank) its Morton index -> balanced work split
+//   ipb  : per active parent (by rank) palette-advance prefix, level-relative
+//   list : per active parent (by rank) its Morton index
+//   pend : one bit per child of the level: "same-level chain not resolved yet"
 // IdxT is u16 in the shared-memory variant (L <= 5: <= 4096 parents, <= 32768
 // entries per level) and u32 in the global-workspace variant (L = 6, 7).
 __host__ __device__ __forceinline__ uint32_t levoffA(int j) {
     return j == 0 ? 0u : 4u + ((1u << (3 * j)) - 8u) / 7u;
 }
 struct Layout {
-    uint32_t lev, mask, wpre, ipb, list, words, W;   // offsets in u32 units
+    uint32_t lev, mask, wpre, ipb, list, pend, words, W;   // offsets in u32 units
 };
 __host__ __device__ inline Layout make_layout(int L, int idx_bytes) {
     Layout Y;
@@ -344,7 +345,8 @@ __host__ __device__ inline Layout make_layout(int L, int idx_bytes) {
     Y.ipb = (Y.wpre + Y.W + 1 + 3) & ~3u;
     uint32_t idx_words = (maxP * idx_bytes + 15) / 16 * 4;
     Y.list = Y.ipb + idx_words;
-    Y.words = Y.list + idx_words;
+    Y.pend = Y.list + idx_words;
+    Y.words = Y.pend + (8 * maxP + 31) / 32;
     return Y;
 }
 
@@ -410,150 +412,31 @@ __device__ __forceinline__ uint64_t block_sum64(uint64_t v, int slot, K2Shared& 
     return t;
 }
 
-// Per-level context for child evaluation.
-template <typename IdxT>
-struct LevelCtx {
-    const uint32_t* plev;    // parent level values (Morton)
-    const uint32_t* pmask;   // parent active bitmask
-    const uint32_t* wpre;    // word rank prefix
-    const IdxT* ipb;         // palette-advance prefix per active parent (by rank), level-relative
-    const uint64_t* E8;      // entry groups of this stream
-    uint32_t g0;             // first group of this level (e0 / 8)
-    uint32_t gcap;           // groups inside the stream's entry region
-    const uint32_t* pal;
-    int64_t plen;
-    int64_t ipbase;          // i_p before the level's first entry
-    int cbits;               // bits per axis at the child level
-};
-
-template <typename IdxT>
-__device__ __forceinline__ bool is_active(const LevelCtx<IdxT>& C, uint32_t q) {
-    return (C.pmask[q >> 5] >> (q & 31)) & 1u;
-}
-template <typename IdxT>
-__device__ __forceinline__ uint32_t rank_of(const LevelCtx<IdxT>& C, uint32_t q) {
-    return C.wpre[q >> 5] + __popc(C.pmask[q >> 5] & ((1u << (q & 31)) - 1u));
-}
-template <typename IdxT>
-__device__ __forceinline__ uint64_t load_group(const LevelCtx<IdxT>& C, uint32_t r) {
-    uint32_t g = C.g0 + r;
-    return g < C.gcap ? __ldg(C.E8 + g) : 0ull;
-}
-template <typename IdxT>
-__device__ __forceinline__ uint32_t pal_at(const LevelCtx<IdxT>& C, int64_t idx) {
-    idx = idx < 0 ? 0 : idx;
-    idx = idx >= C.plen ? C.plen - 1 : idx;
-    return __ldg(C.pal + idx);
-}
-
-// Value of same-level node nm (decoded earlier in sequential order, nm < j):
-// inactive parent -> the parent's value; otherwise its own entry.  Every
-// even-coordinate hop turns one more coordinate odd, so <= 3 hops
-// (codec.py:402-425 applied transitively).
-template <typename IdxT>
-__device__ __noinline__ uint32_t neighbor_value(const LevelCtx<IdxT>& C, uint32_t nm) {
-    for (int hop = 0; hop < 4; ++hop) {
-        uint32_t q = nm >> 3;
-        int c = nm & 7;
-        if (!is_active(C, q)) return C.plev[q];
-        uint32_t r = rank_of(C, q);
-        uint64_t w = load_group(C, r);
-        uint32_t e = (uint32_t)(w >> (8 * c)) & 0xFFu;
-        uint32_t op = e & 7u;
-        if (op == 0) return C.plev[q];
-        if (op <= 3) {
-            int a = op - 1;
-            uint32_t M = axis_mask(a, C.cbits);
-            uint32_t part = nm & M;
-            if ((c >> a) & 1) {
-                if (part == M) return 0;
-                return C.plev[((((part | ~M) + 1u) & M) | (nm & ~M)) >> 3];
-            }
-            if (part == 0) return 0;
-            nm = ((part - 1u) & M) | (nm & ~M);
-            continue;
-        }
-        if (op == 7) return 0;
-        int64_t ip = C.ipbase + (int64_t)C.ipb[r] + prefix_bytes(op_eq(w, 6), c);
-        int64_t idx = op == 4 ? ip : (op == 5 ? ip - (int64_t)(e >> 4) - 1 : ip + 1);
-        return pal_at(C, idx);
-    }
-    return 0;
-}
-
-// One child of active parent q (entries w, palette-advance base ipq).  Records
-// op-specific errors (priority 2) in myerr when the entry is valid.
-template <typename IdxT>
-__device__ __forceinline__ uint32_t child_value(const LevelCtx<IdxT>& C, uint32_t q, int c, uint64_t w, uint32_t pv,
-                                                int64_t ipq, uint64_t pa, uint32_t ent, uint32_t nvalid,
-                                                unsigned long long& myerr) {
-    const uint32_t e = (uint32_t)(w >> (8 * c)) & 0xFFu;
-    const uint32_t op = e & 7u;
-    if (op == 0 || op == 7) return pv;
-    int st = 0;
-    uint32_t val = pv;
-    if (op <= 3) {
-        const int a = op - 1;
-        const uint32_t j = (q << 3) | c;
-        const uint32_t M = axis_mask(a, C.cbits);
-        const uint32_t part = j & M;
-        if ((c >> a) & 1) {      // odd: the +1 neighbour is decoded later -> its parent's value
-            if (part == M) st = CSV_ST_BAD_NEIGHBOR;
-            else val = C.plev[((((part | ~M) + 1u) & M) | (j & ~M)) >> 3];
-        } else {                 // even: the -1 neighbour, same level
-            if (part == 0) st = CSV_ST_BAD_NEIGHBOR;
-            else val = neighbor_value(C, ((part - 1u) & M) | (j & ~M));
-        }
-    } else {
-        const int64_t ip = ipq + prefix_bytes(pa, c);
-        int64_t idx;
-        if (op == 4) idx = ip;
-        else if (op == 5) { idx = ip - (int64_t)(e >> 4) - 1; if (idx < 0) st = CSV_ST_DELTA_RANGE; }
-        else { idx = ip + 1; if (idx >= C.plen) st = CSV_ST_PALETTE_RANGE; }
-        val = pal_at(C, idx);
-    }
-    if (st && ent < nvalid) {
-        unsigned long long k = ekey(ent, 2, st);
-        myerr = k < myerr ? k : myerr;
-    }
-    return val;
-}
-
-// BAD_OP / LEAF_STOP of a whole group at once (SWAR over the 8 entry bytes).
-__device__ __forceinline__ unsigned long long group_flag_errors(uint64_t w, uint32_t e_first, uint32_t nvalid, bool leaf) {
-    const uint64_t ones = 0x0101010101010101ull;
-    uint64_t valid = e_first >= nvalid ? 0ull : (nvalid - e_first >= 8 ? ~0ull : ((1ull << (8 * (nvalid - e_first))) - 1ull));
-    uint64_t b7 = op_eq(w, 7) & valid;
-    uint64_t st = leaf ? (((w >> 3) & ones) & valid & ~b7) : 0ull;
-    if (!(b7 | st)) return ~0ull;
-    unsigned long long k = ~0ull;
-    if (b7) k = ekey(e_first + (__ffsll((long long)b7) - 1) / 8, 0, CSV_ST_BAD_OP);
-    if (st) {
-        unsigned long long k2 = ekey(e_first + (__ffsll((long long)st) - 1) / 8, 1, CSV_ST_LEAF_STOP);
-        k = k2 < k ? k2 : k;
-    }
-    return k;
-}
-
 struct RasterCtx {
-    uint32_t* base;     // voxel (bx*side, by*side, bz*side) of the slab, may be out of slab
+    uint32_t* base;     // voxel (ox, oy, oz) of the slab (valid when fast)
     int64_t ox, oy, oz; // brick origin (LOD-t voxels)
     int64_t cx, cy;     // row pitch / plane
     int64_t zb, ze;
     bool fast;          // brick fully inside crop and slab, 8-byte aligned rows
 };
 
+// Address of brick-local voxel (x, y, z) in the raster slab, or nullptr if cropped away.
+__device__ __forceinline__ uint32_t* raster_ptr(const RasterCtx& R, const Plan& P, int64_t x, int64_t y, int64_t z) {
+    if (R.fast) return R.base + (z * R.cy + y) * R.cx + x;
+    int64_t gz = R.oz + z, gy = R.oy + y, gx = R.ox + x;
+    if (gz < R.zb || gz >= R.ze || gy >= R.cy || gx >= R.cx) return nullptr;
+    return P.out + ((gz - R.zb) * R.cy + gy) * R.cx + gx;
+}
+
 __device__ __forceinline__ void store_pair(const RasterCtx& R, const Plan& P, int64_t x, int64_t y, int64_t z,
                                            uint32_t a, uint32_t b) {
     if (R.fast) {
-        uint32_t* p = R.base + (z * R.cy + y) * R.cx + x;
-        *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
+        *reinterpret_cast<uint2*>(R.base + (z * R.cy + y) * R.cx + x) = make_uint2(a, b);
         return;
     }
-    int64_t gz = R.oz + z, gy = R.oy + y, gx = R.ox + x;
-    if (gz < R.zb || gz >= R.ze || gy >= R.cy || gx >= R.cx) return;
-    uint32_t* p = P.out + ((gz - R.zb) * R.cy + gy) * R.cx + gx;
-    if (gx + 1 < R.cx) {
+    uint32_t* p = raster_ptr(R, P, x, y, z);
+    if (!p) return;
+    if (R.ox + x + 1 < R.cx) {
         if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
         else { p[0] = a; p[1] = b; }
     } else {
@@ -577,18 +460,28 @@ __device__ void fill_output(const VolView& V, const Plan& P, const RasterCtx& R,
     const uint64_t n = 1ull << (3 * lb);
     if (MODE == OUT_MORTON) {
         for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) out_m[i] = val;
+    } else if (lb == 0) {
+        if (threadIdx.x == 0) {
+            uint32_t* p = raster_ptr(R, P, 0, 0, 0);
+            if (p) *p = val;
+        }
     } else {
         const int side = 1 << lb;
         for (uint64_t i = threadIdx.x; i < n / 2; i += blockDim.x) {
             int64_t x = (2 * i) & (side - 1), y = ((2 * i) >> lb) & (side - 1), z = (2 * i) >> (2 * lb);
-            if (side == 1) { x = 0; y = 0; z = 0; }
             store_pair(R, P, x, y, z, val, val);
         }
-        if (side == 1 && threadIdx.x == 0) {
-            if (R.oz >= R.zb && R.oz < R.ze && R.oy < R.cy && R.ox < R.cx)
-                P.out[((R.oz - R.zb) * R.cy + R.oy) * R.cx + R.ox] = val;
-        }
     }
+}
+
+// Storage slot of child j of the current level: shared level array, raster
+// voxel or Morton pool entry.  nullptr when the voxel is cropped away.
+template <int MODE>
+__device__ __forceinline__ uint32_t* child_slot(bool final_level, uint32_t* clev, uint32_t* out_m, const RasterCtx& R,
+                                                const Plan& P, uint32_t j) {
+    if (!final_level) return clev + j;
+    if (MODE == OUT_MORTON) return out_m + j;
+    return raster_ptr(R, P, compact3(j), compact3(j >> 1), compact3(j >> 2));
 }
 
 template <int MODE, bool SMEM>
@@ -604,7 +497,10 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
     uint32_t* wpre = ws + Y.wpre;
     IdxT* ipb = reinterpret_cast<IdxT*>(ws + Y.ipb);
     IdxT* list = reinterpret_cast<IdxT*>(ws + Y.list);
+    uint32_t* pend = ws + Y.pend;
     const int N = V.N;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
     for (uint64_t r = blockIdx.x; r < P.n; r += gridDim.x) {
         const uint64_t b = req_local(V, P, r);
         const int t = req_lod(P, r);
@@ -646,7 +542,6 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
         }
         const csv_stream_result src = P.sres[2 * r], srd = P.sres[2 * r + 1];
         const uint64_t eo0 = P.eoff[2 * r], eo1 = P.eoff[2 * r + 1], eo2 = P.eoff[2 * r + 2];
-        const Layout& Yl = Y;
         if (threadIdx.x == 0) {
             lev[0] = __ldg(pal);      // root (codec.py:353)
             mask0[0] = 1u;
@@ -663,31 +558,26 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
             const bool final_level = (l - 1 == t);
             const uint32_t Pn = 1u << (3 * (N - l));
             const uint32_t W = (Pn + 31) >> 5;
-            uint32_t* pmask = mask0 + cur * Yl.W;
-            uint32_t* cmask = mask0 + (cur ^ 1) * Yl.W;
+            const uint32_t PW = (8 * Pn + 31) >> 5;      // pending words (children)
+            uint32_t* pmask = mask0 + cur * Y.W;
+            uint32_t* cmask = mask0 + (cur ^ 1) * Y.W;
             const csv_stream_result& sr = leaf ? srd : src;
             const uint32_t e0 = leaf ? cur_d : cur_c;
-            // (A) rank prefix of active parents
+            const uint8_t* Eb = P.entries + (leaf ? eo1 : eo0);          // this stream's entry bytes
+            const uint32_t ecap = (uint32_t)((leaf ? eo2 : eo1) - (leaf ? eo1 : eo0));
+            const uint32_t* plev = lev + levoffA(N - l);
+            uint32_t* clev = final_level ? nullptr : lev + levoffA(N - l + 1);
+            const int cbits = N - l + 1;
+            // (A) rank prefix of active parents; clear pending bits
             for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
                 uint32_t mw = pmask[i];
                 if (Pn < 32) mw &= (1u << Pn) - 1u;
                 pmask[i] = mw;
                 wpre[i] = __popc(mw);
             }
+            for (uint32_t i = threadIdx.x; i < PW; i += blockDim.x) pend[i] = 0;
             __syncthreads();
             const uint32_t nact = block_scan_inplace(wpre, W, S);
-            LevelCtx<IdxT> C;
-            C.plev = lev + levoffA(N - l);
-            C.pmask = pmask;
-            C.wpre = wpre;
-            C.ipb = ipb;
-            C.E8 = reinterpret_cast<const uint64_t*>(P.entries + (leaf ? eo1 : eo0));
-            C.g0 = e0 >> 3;
-            C.gcap = (uint32_t)(((leaf ? eo2 : eo1) - (leaf ? eo1 : eo0)) >> 3);
-            C.pal = pal;
-            C.plen = plen;
-            C.ipbase = ipbase;
-            C.cbits = N - l + 1;
             // (B) active list + palette-advance counts per active parent
             for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
                 uint32_t mw = pmask[i], rk = wpre[i];
@@ -699,7 +589,8 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
             }
             uint64_t pdl = 0;
             for (uint32_t i = threadIdx.x; i < nact; i += blockDim.x) {
-                uint64_t w = load_group(C, i);
+                const uint32_t off = e0 + 8 * i;
+                uint64_t w = off + 8 <= ecap ? __ldg(reinterpret_cast<const uint64_t*>(Eb + off)) : 0ull;
                 ipb[i] = (IdxT)__popcll(op_eq(w, 6));
                 pdl += __popcll(op_eq(w, 5));
             }
@@ -707,46 +598,61 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
             __syncthreads();
             const uint32_t tot_pa = block_scan_inplace(ipb, nact, S);
             const uint32_t nvalid = sr.n_entries;
-            // (C1) active parents, balanced by rank
+            // (C1) one lane per child of an active parent (8 consecutive lanes = one parent)
+            const uint32_t nch = 8 * nact;
             unsigned long long myerr = ~0ull;
-            uint32_t* clev = final_level ? nullptr : lev + levoffA(N - l + 1);
-            for (uint32_t rk = threadIdx.x; rk < nact; rk += blockDim.x) {
-                const uint32_t q = list[rk];
-                const uint64_t w = load_group(C, rk);
-                const uint32_t ent0 = e0 + 8 * rk;
-                const uint32_t pv = C.plev[q];
-                const int64_t ipq = ipbase + (int64_t)ipb[rk];
-                const uint64_t pa = op_eq(w, 6);
-                unsigned long long fe = group_flag_errors(w, ent0, nvalid, leaf);
-                myerr = fe < myerr ? fe : myerr;
-                if (final_level && MODE == OUT_RASTER) {
-                    const int pb = N - l;
-                    const int64_t x0 = 2 * (int64_t)compact3(q), y0 = 2 * (int64_t)compact3(q >> 1),
-                                  z0 = 2 * (int64_t)compact3(q >> 2);
-                    (void)pb;
-#pragma unroll 1
-                    for (int row = 0; row < 4; ++row) {
-                        const int c0 = 2 * row;
-                        uint32_t a = child_value(C, q, c0, w, pv, ipq, pa, ent0 + c0, nvalid, myerr);
-                        uint32_t bb = child_value(C, q, c0 + 1, w, pv, ipq, pa, ent0 + c0 + 1, nvalid, myerr);
-                        store_pair(R, P, x0, y0 + (row & 1), z0 + (row >> 1), a, bb);
+            for (uint32_t kb = threadIdx.x - lane; kb < nch; kb += blockDim.x) {
+                const uint32_t k = kb + lane;
+                const bool valid = k < nch;
+                const uint32_t rk = k >> 3;
+                const int c = k & 7;
+                const uint32_t q = valid ? (uint32_t)list[rk] : 0u;
+                const uint32_t ent = e0 + k;
+                const uint32_t e = (valid && ent < ecap) ? (uint32_t)__ldg(Eb + ent) : 0u;
+                const uint32_t op = e & 7u;
+                const uint32_t pv = plev[q];
+                const uint32_t seg = 0xFFu << (lane & 24);
+                const uint32_t pam = __ballot_sync(FULL, valid && op == 6u);
+                const uint32_t nstop = __ballot_sync(FULL, valid && !(e & 8u));
+                uint32_t val = pv;
+                int st = 0;
+                bool chain = false;
+                const uint32_t j = (q << 3) | c;
+                if (op >= 1 && op <= 3) {
+                    const int a = op - 1;
+                    const uint32_t M = axis_mask(a, cbits);
+                    const uint32_t part = j & M;
+                    if ((c >> a) & 1) {      // odd: the +1 neighbour is decoded later -> its parent's value
+                        if (part == M) st = CSV_ST_BAD_NEIGHBOR;
+                        else val = plev[((((part | ~M) + 1u) & M) | (j & ~M)) >> 3];
+                    } else {                 // even: the -1 neighbour at this level (resolved in rounds)
+                        if (part == 0) st = CSV_ST_BAD_NEIGHBOR;
+                        else chain = true;
                     }
-                } else {
-                    uint32_t v[8];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) v[c] = child_value(C, q, c, w, pv, ipq, pa, ent0 + c, nvalid, myerr);
-                    uint32_t* dstp = final_level ? out_m + 8ull * q : clev + 8 * q;
-                    if (!final_level || ((reinterpret_cast<uintptr_t>(dstp) & 15) == 0)) {
-                        reinterpret_cast<uint4*>(dstp)[0] = make_uint4(v[0], v[1], v[2], v[3]);
-                        reinterpret_cast<uint4*>(dstp)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+                } else if (op >= 4 && op <= 6) {
+                    const int64_t ip = ipbase + (int64_t)ipb[valid ? rk : 0] + __popc(pam & seg & ((1u << lane) - 1u));
+                    int64_t idx;
+                    if (op == 4) idx = ip;
+                    else if (op == 5) { idx = ip - (int64_t)(e >> 4) - 1; if (idx < 0) st = CSV_ST_DELTA_RANGE; }
+                    else { idx = ip + 1; if (idx >= (int64_t)plen) st = CSV_ST_PALETTE_RANGE; }
+                    idx = idx < 0 ? 0 : (idx >= (int64_t)plen ? (int64_t)plen - 1 : idx);
+                    val = __ldg(pal + idx);
+                }
+                if (valid && ent < nvalid) {
+                    unsigned long long kk = ~0ull;
+                    if (op == 7) kk = ekey(ent, 0, CSV_ST_BAD_OP);
+                    else if (leaf && (e & 8u)) kk = ekey(ent, 1, CSV_ST_LEAF_STOP);
+                    else if (st) kk = ekey(ent, 2, st);
+                    myerr = kk < myerr ? kk : myerr;
+                }
+                if (!final_level && valid && c == 0)
+                    reinterpret_cast<uint8_t*>(cmask)[q] = (uint8_t)(nstop >> (lane & 24));
+                if (valid) {
+                    if (chain) {
+                        atomicOr(&pend[j >> 5], 1u << (j & 31));
                     } else {
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) dstp[c] = v[c];
-                    }
-                    if (!final_level) {
-                        // stop bits -> inactive children (codec.py:460-463), packed to one byte
-                        uint64_t st = (w >> 3) & 0x0101010101010101ull;
-                        reinterpret_cast<uint8_t*>(cmask)[q] = (uint8_t)(~(uint32_t)((st * 0x0102040810204080ull) >> 56));
+                        uint32_t* slot = child_slot<MODE>(final_level, clev, out_m, R, P, j);
+                        if (slot) *slot = val;
                     }
                 }
             }
@@ -758,16 +664,16 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
                 for (uint32_t i = threadIdx.x; i < Pn; i += blockDim.x) {
                     const uint32_t qx = i & pm, qy = (i >> pb) & pm, qz = i >> (2 * pb);
                     const uint32_t q = spread3_u32(qx) | (spread3_u32(qy) << 1) | (spread3_u32(qz) << 2);
-                    if (is_active(C, q)) continue;
-                    const uint32_t pv = C.plev[q];
+                    if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
+                    const uint32_t pv = plev[q];
 #pragma unroll
                     for (int row = 0; row < 4; ++row)
                         store_pair(R, P, 2 * qx, 2 * qy + (row & 1), 2 * qz + (row >> 1), pv, pv);
                 }
             } else {
                 for (uint32_t q = threadIdx.x; q < Pn; q += blockDim.x) {
-                    if (is_active(C, q)) continue;
-                    const uint32_t pv = C.plev[q];
+                    if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
+                    const uint32_t pv = plev[q];
                     uint32_t* dstp = final_level ? out_m + 8ull * q : clev + 8 * q;
                     if (!final_level || ((reinterpret_cast<uintptr_t>(dstp) & 15) == 0)) {
                         reinterpret_cast<uint4*>(dstp)[0] = make_uint4(pv, pv, pv, pv);
@@ -799,10 +705,9 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
                     }
                 } else {
                     // nibble index of entry `ent` = ent + #payload nibbles before it
-                    const uint64_t* E8 = C.E8;
                     uint64_t cnt = 0;
                     for (uint32_t g = threadIdx.x; g < (ent + 7) / 8; g += blockDim.x) {
-                        uint64_t w = (g < C.gcap) ? __ldg(E8 + g) : 0ull;
+                        uint64_t w = (8 * g + 8 <= ecap) ? __ldg(reinterpret_cast<const uint64_t*>(Eb) + g) : 0ull;
                         uint32_t lim = ent - 8 * g;
                         uint64_t m = op_eq(w, 5);
                         if (lim < 8) m &= (1ull << (8 * lim)) - 1ull;
@@ -815,6 +720,37 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
                 write_result(P, r, st, leaf ? 1 : 0, pos, 0, 0);
                 failed = true;
                 break;
+            }
+            // (R) same-level chains (codec.py:422-423, nm < j): a child copies its -1
+            // neighbour once that one is final.  Hops make coordinates odd, so a
+            // chain is at most 3 deep and resolves within 3 rounds.
+            for (int round = 0; round < 4; ++round) {
+                int any = 0;
+                for (uint32_t wdx = threadIdx.x; wdx < PW; wdx += blockDim.x) {
+                    uint32_t bits = *(volatile uint32_t*)&pend[wdx];
+                    while (bits) {
+                        const int bit = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const uint32_t j = 32 * wdx + bit;
+                        const uint32_t q = j >> 3;
+                        const int c = j & 7;
+                        const uint32_t rk = wpre[q >> 5] + __popc(pmask[q >> 5] & ((1u << (q & 31)) - 1u));
+                        const uint32_t e = __ldg(Eb + e0 + 8 * rk + c);
+                        const int a = (int)(e & 7u) - 1;
+                        const uint32_t M = axis_mask(a, cbits);
+                        const uint32_t nm = (((j & M) - 1u) & M) | (j & ~M);
+                        if ((*(volatile uint32_t*)&pend[nm >> 5] >> (nm & 31)) & 1u) { any = 1; continue; }
+                        __threadfence_block();
+                        uint32_t* dst = child_slot<MODE>(final_level, clev, out_m, R, P, j);
+                        if (dst) {
+                            const uint32_t* srcp = child_slot<MODE>(final_level, clev, out_m, R, P, nm);
+                            *(volatile uint32_t*)dst = *(volatile const uint32_t*)srcp;
+                        }
+                        __threadfence_block();
+                        atomicAnd(&pend[j >> 5], ~(1u << (j & 31)));
+                    }
+                }
+                if (!__syncthreads_or(any)) break;
             }
             if (leaf) cur_d = e0 + 8 * nact; else cur_c = e0 + 8 * nact;
             ipbase += tot_pa;
