@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_streams(VolView V, Plan P, unsi
 }
 
 // ============================================================================ K2: replay
-// Shared (or global-workspace) layout for one brick, sized for L = N - t levels:
+// Per-brick working set, sized for LMAX = N - t levels (compile-time):
 //   lev  : values of levels t+1..N in Morton order; level N-j at levoffA(j)
 //          (16-byte aligned for j >= 1)
 //   mask : 2 x W words, active-parent bitmask ping-pong
@@ -326,16 +326,17 @@ __global__ void __launch_bounds__(K1_THREADS) k1_streams(VolView V, Plan P, unsi
 //   ipb  : per active parent (by rank) palette-advance prefix, level-relative
 //   list : per active parent (by rank) its Morton index
 //   pend : one bit per child of the level: "same-level chain not resolved yet"
-// IdxT is u16 in the shared-memory variant (L <= 5: <= 4096 parents, <= 32768
-// entries per level) and u32 in the global-workspace variant (L = 6, 7).
-__host__ __device__ __forceinline__ uint32_t levoffA(int j) {
+// LMAX <= 5 lives in shared memory with 16-bit ipb/list (<= 4096 parents and
+// <= 32768 entries per level); LMAX 6, 7 (b = 64, 128 at fine LODs) use a
+// per-CTA global workspace with 32-bit indices.
+__host__ __device__ constexpr uint32_t levoffA(int j) {
     return j == 0 ? 0u : 4u + ((1u << (3 * j)) - 8u) / 7u;
 }
 struct Layout {
     uint32_t lev, mask, wpre, ipb, list, pend, words, W;   // offsets in u32 units
 };
-__host__ __device__ inline Layout make_layout(int L, int idx_bytes) {
-    Layout Y;
+__host__ __device__ constexpr Layout make_layout(int L, int idx_bytes) {
+    Layout Y{};
     uint32_t nlev = levoffA(L);
     uint32_t maxP = 1u << (3 * (L - 1));
     Y.W = (maxP + 31) / 32;
@@ -363,6 +364,8 @@ struct K2Shared {
     unsigned long long errkey;
     uint32_t scan[K2_WARPS + 1];
     uint64_t red64[2][K2_WARPS];
+    uint32_t lut_lo[512];    // raster offset of the low 3 Morton bit-triples (x + y*cx + z*plane)
+    uint32_t lut_hi[64];     // ... of the next 2 triples (scaled by 8)
 };
 
 // Block-wide in-place exclusive scan of arr[0..n); returns the total.
@@ -412,36 +415,21 @@ __device__ __forceinline__ uint64_t block_sum64(uint64_t v, int slot, K2Shared& 
     return t;
 }
 
-struct RasterCtx {
-    uint32_t* base;     // voxel (ox, oy, oz) of the slab (valid when fast)
-    int64_t ox, oy, oz; // brick origin (LOD-t voxels)
-    int64_t cx, cy;     // row pitch / plane
-    int64_t zb, ze;
-    bool fast;          // brick fully inside crop and slab, 8-byte aligned rows
+// Raster placement of one brick at LOD t (replaces morton_to_grid + slice
+// assignment, container.py:465-468).  Fast bricks (fully inside crop and slab,
+// even row pitch, 15-bit Morton indices) address voxels through the per-CTA
+// LUT with 32-bit offsets from `base`; edge bricks take the general path.
+struct Raster {
+    uint32_t* base;     // voxel (ox, oy, oz) of the slab
+    int64_t ox, oy, oz; // brick origin in LOD-t voxels
+    bool fast;
 };
 
-// Address of brick-local voxel (x, y, z) in the raster slab, or nullptr if cropped away.
-__device__ __forceinline__ uint32_t* raster_ptr(const RasterCtx& R, const Plan& P, int64_t x, int64_t y, int64_t z) {
-    if (R.fast) return R.base + (z * R.cy + y) * R.cx + x;
-    int64_t gz = R.oz + z, gy = R.oy + y, gx = R.ox + x;
-    if (gz < R.zb || gz >= R.ze || gy >= R.cy || gx >= R.cx) return nullptr;
-    return P.out + ((gz - R.zb) * R.cy + gy) * R.cx + gx;
-}
-
-__device__ __forceinline__ void store_pair(const RasterCtx& R, const Plan& P, int64_t x, int64_t y, int64_t z,
-                                           uint32_t a, uint32_t b) {
-    if (R.fast) {
-        *reinterpret_cast<uint2*>(R.base + (z * R.cy + y) * R.cx + x) = make_uint2(a, b);
-        return;
-    }
-    uint32_t* p = raster_ptr(R, P, x, y, z);
-    if (!p) return;
-    if (R.ox + x + 1 < R.cx) {
-        if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
-        else { p[0] = a; p[1] = b; }
-    } else {
-        p[0] = a;
-    }
+__device__ __forceinline__ uint32_t* raster_slot(const Raster& R, const Plan& P, const K2Shared& S, uint32_t j) {
+    if (R.fast) return R.base + (S.lut_lo[j & 511] + S.lut_hi[j >> 9]);
+    int64_t gx = R.ox + compact3(j), gy = R.oy + compact3(j >> 1), gz = R.oz + compact3(j >> 2);
+    if (gz < P.z_begin || gz >= P.z_end || gy >= P.cy || gx >= P.cx) return nullptr;
+    return P.out + ((gz - P.z_begin) * P.cy + gy) * P.cx + gx;
 }
 
 __device__ __forceinline__ void write_result(const Plan& P, uint64_t r, int st, int stream, int64_t pos,
@@ -455,77 +443,71 @@ __device__ __forceinline__ void write_result(const Plan& P, uint64_t r, int st, 
 
 // Fill the whole output of request r with one value (relevant == 0, codec.py:353-358).
 template <int MODE>
-__device__ void fill_output(const VolView& V, const Plan& P, const RasterCtx& R, int t, uint32_t* out_m, uint32_t val) {
-    const int lb = V.N - t;
-    const uint64_t n = 1ull << (3 * lb);
+__device__ void fill_output(int lb, const Plan& P, const Raster& R, const K2Shared& S, uint32_t* out_m, uint32_t val) {
+    const uint32_t n = 1u << (3 * lb);
     if (MODE == OUT_MORTON) {
-        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) out_m[i] = val;
-    } else if (lb == 0) {
-        if (threadIdx.x == 0) {
-            uint32_t* p = raster_ptr(R, P, 0, 0, 0);
-            if (p) *p = val;
-        }
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out_m[i] = val;
     } else {
-        const int side = 1 << lb;
-        for (uint64_t i = threadIdx.x; i < n / 2; i += blockDim.x) {
-            int64_t x = (2 * i) & (side - 1), y = ((2 * i) >> lb) & (side - 1), z = (2 * i) >> (2 * lb);
-            store_pair(R, P, x, y, z, val, val);
+        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
+            uint32_t* p = raster_slot(R, P, S, j);
+            if (p) *p = val;
         }
     }
 }
 
-// Storage slot of child j of the current level: shared level array, raster
-// voxel or Morton pool entry.  nullptr when the voxel is cropped away.
-template <int MODE>
-__device__ __forceinline__ uint32_t* child_slot(bool final_level, uint32_t* clev, uint32_t* out_m, const RasterCtx& R,
-                                                const Plan& P, uint32_t j) {
-    if (!final_level) return clev + j;
-    if (MODE == OUT_MORTON) return out_m + j;
-    return raster_ptr(R, P, compact3(j), compact3(j >> 1), compact3(j >> 2));
-}
-
-template <int MODE, bool SMEM>
-__global__ void __launch_bounds__(K2_THREADS, SMEM ? 5 : 1)
-k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
+template <int MODE, int LMAX>
+__global__ void __launch_bounds__(K2_THREADS, LMAX <= 5 ? 5 : 1)
+k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
+    constexpr bool SMEM = LMAX <= 5;
     using IdxT = typename std::conditional<SMEM, uint16_t, uint32_t>::type;
+    constexpr Layout Y = make_layout(LMAX, sizeof(IdxT));
     extern __shared__ __align__(16) uint32_t dsm[];
     __shared__ K2Shared S;
-    const Layout Y = make_layout(Lmax, sizeof(IdxT));
-    uint32_t* ws = SMEM ? dsm : gws + blockIdx.x * ws_stride;
-    uint32_t* lev = ws + Y.lev;
-    uint32_t* mask0 = ws + Y.mask;
-    uint32_t* wpre = ws + Y.wpre;
-    IdxT* ipb = reinterpret_cast<IdxT*>(ws + Y.ipb);
-    IdxT* list = reinterpret_cast<IdxT*>(ws + Y.list);
-    uint32_t* pend = ws + Y.pend;
+    uint32_t* ws;
+    if constexpr (SMEM) ws = dsm;
+    else ws = gws + blockIdx.x * ws_stride;
+    uint32_t* const lev = ws + Y.lev;
+    uint32_t* const mask0 = ws + Y.mask;
+    uint32_t* const wpre = ws + Y.wpre;
+    IdxT* const ipb = reinterpret_cast<IdxT*>(ws + Y.ipb);
+    IdxT* const list = reinterpret_cast<IdxT*>(ws + Y.list);
+    uint32_t* const pend = ws + Y.pend;
     const int N = V.N;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+    if (MODE == OUT_RASTER) {
+        // Morton -> raster offset tables for this launch's pitches
+        const uint32_t cx = (uint32_t)P.cx, plane = (uint32_t)(P.cx * P.cy);
+        for (uint32_t m = threadIdx.x; m < 512 + 64; m += blockDim.x) {
+            uint32_t mm = m < 512 ? m : m - 512, sc = m < 512 ? 1u : 8u;
+            uint32_t off = sc * (compact3(mm) + compact3(mm >> 1) * cx + compact3(mm >> 2) * plane);
+            if (m < 512) S.lut_lo[mm] = off; else S.lut_hi[mm] = off;
+        }
+        __syncthreads();
+    }
     for (uint64_t r = blockIdx.x; r < P.n; r += gridDim.x) {
         const uint64_t b = req_local(V, P, r);
         const int t = req_lod(P, r);
         if (b >= V.nb || t > N) { write_result(P, r, -1, 0, 0, 0, 0); continue; }
-        if (t < N && N - t > Lmax) continue;           // belongs to the other variant
+        if (t < N && N - t > LMAX) continue;            // served by a larger instantiation
         if (!SMEM && N - t <= 5) continue;
         uint32_t* out_m = MODE == OUT_MORTON ? P.out + P.dst[r] : nullptr;
         const uint32_t plen = V.pal_len[b];
         const uint32_t* pal = V.palette + V.pal_off[b];
-        RasterCtx R{};
+        Raster R{};
         if (MODE == OUT_RASTER) {
             const uint64_t gb = V.brick_begin + b;
             const int64_t side = 1ll << (N - t);
             R.ox = (int64_t)(gb % V.gx) * side;
             R.oy = (int64_t)((gb / V.gx) % V.gy) * side;
             R.oz = (int64_t)(gb / (V.gx * V.gy)) * side;
-            R.cx = P.cx; R.cy = P.cy; R.zb = P.z_begin; R.ze = P.z_end;
-            R.base = P.out + ((R.oz - R.zb) * R.cy + R.oy) * R.cx + R.ox;
-            R.fast = side >= 2 && R.ox + side <= R.cx && R.oy + side <= R.cy && R.oz >= R.zb && R.oz + side <= R.ze &&
-                     (R.cx & 1) == 0 && ((reinterpret_cast<uintptr_t>(P.out) & 7) == 0);
+            R.base = P.out + ((R.oz - P.z_begin) * P.cy + R.oy) * P.cx + R.ox;
+            R.fast = N - t <= 5 && R.ox + side <= P.cx && R.oy + side <= P.cy && R.oz >= P.z_begin &&
+                     R.oz + side <= P.z_end && (uint64_t)P.cx * P.cy * side < (1ull << 32);
         }
         if (plen == 0) { write_result(P, r, CSV_ST_EMPTY_PALETTE, 0, 0, 0, 0); continue; }
         if (t == N) {   // coarsest LOD: palette[0] (codec.py:514-516, container.py:178-182)
-            if (MODE == OUT_MORTON) { if (threadIdx.x == 0) out_m[0] = __ldg(pal); }
-            else fill_output<MODE>(V, P, R, t, nullptr, __ldg(pal));
+            fill_output<MODE>(0, P, R, S, out_m, __ldg(pal));
             write_result(P, r, 0, 0, 0, 0, 0);
             continue;
         }
@@ -536,7 +518,7 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
             if (t == 0 && nd_raw > 0 && V.d_bytes[b] < 4) { write_result(P, r, CSV_ST_UNDERRUN, 1, 0, 0, 0); continue; }
         }
         if ((uint64_t)nc + nd == 0) {
-            fill_output<MODE>(V, P, R, t, out_m, __ldg(pal));
+            fill_output<MODE>(N - t, P, R, S, out_m, __ldg(pal));
             write_result(P, r, 0, 0, 0, 0, 0);
             continue;
         }
@@ -550,7 +532,7 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
         __syncthreads();
         uint32_t cur_c = 0, cur_d = 0;
         uint64_t pd_c = 0, pd_d = 0;
-        int64_t ipbase = 0;
+        int32_t ipbase = 0;
         int cur = 0;
         bool failed = false;
         for (int l = N; l > t; --l) {
@@ -559,15 +541,16 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
             const uint32_t Pn = 1u << (3 * (N - l));
             const uint32_t W = (Pn + 31) >> 5;
             const uint32_t PW = (8 * Pn + 31) >> 5;      // pending words (children)
-            uint32_t* pmask = mask0 + cur * Y.W;
-            uint32_t* cmask = mask0 + (cur ^ 1) * Y.W;
-            const csv_stream_result& sr = leaf ? srd : src;
+            uint32_t* const pmask = mask0 + cur * Y.W;
+            uint8_t* const cmask = reinterpret_cast<uint8_t*>(mask0 + (cur ^ 1) * Y.W);
+            const csv_stream_result sr = leaf ? srd : src;
             const uint32_t e0 = leaf ? cur_d : cur_c;
-            const uint8_t* Eb = P.entries + (leaf ? eo1 : eo0);          // this stream's entry bytes
+            const uint8_t* const Eb = P.entries + (leaf ? eo1 : eo0);   // this stream's entry bytes
             const uint32_t ecap = (uint32_t)((leaf ? eo2 : eo1) - (leaf ? eo1 : eo0));
-            const uint32_t* plev = lev + levoffA(N - l);
-            uint32_t* clev = final_level ? nullptr : lev + levoffA(N - l + 1);
+            const uint32_t* const plev = lev + levoffA(N - l);
+            uint32_t* const clev = lev + levoffA(N - l + 1);
             const int cbits = N - l + 1;
+            const uint32_t Mx = axis_mask(0, cbits), My = axis_mask(1, cbits), Mz = axis_mask(2, cbits);
             // (A) rank prefix of active parents; clear pending bits
             for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
                 uint32_t mw = pmask[i];
@@ -582,7 +565,7 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
             for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
                 uint32_t mw = pmask[i], rk = wpre[i];
                 while (mw) {
-                    int bit = __ffs(mw) - 1;
+                    const int bit = __ffs(mw) - 1;
                     mw &= mw - 1;
                     list[rk++] = (IdxT)(32 * i + bit);
                 }
@@ -590,7 +573,7 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
             uint64_t pdl = 0;
             for (uint32_t i = threadIdx.x; i < nact; i += blockDim.x) {
                 const uint32_t off = e0 + 8 * i;
-                uint64_t w = off + 8 <= ecap ? __ldg(reinterpret_cast<const uint64_t*>(Eb + off)) : 0ull;
+                const uint64_t w = off + 8 <= ecap ? __ldg(reinterpret_cast<const uint64_t*>(Eb + off)) : 0ull;
                 ipb[i] = (IdxT)__popcll(op_eq(w, 6));
                 pdl += __popcll(op_eq(w, 5));
             }
@@ -600,89 +583,95 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
             const uint32_t nvalid = sr.n_entries;
             // (C1) one lane per child of an active parent (8 consecutive lanes = one parent)
             const uint32_t nch = 8 * nact;
-            unsigned long long myerr = ~0ull;
             for (uint32_t kb = threadIdx.x - lane; kb < nch; kb += blockDim.x) {
                 const uint32_t k = kb + lane;
                 const bool valid = k < nch;
                 const uint32_t rk = k >> 3;
-                const int c = k & 7;
+                const uint32_t c = k & 7;
                 const uint32_t q = valid ? (uint32_t)list[rk] : 0u;
                 const uint32_t ent = e0 + k;
                 const uint32_t e = (valid && ent < ecap) ? (uint32_t)__ldg(Eb + ent) : 0u;
                 const uint32_t op = e & 7u;
-                const uint32_t pv = plev[q];
-                const uint32_t seg = 0xFFu << (lane & 24);
                 const uint32_t pam = __ballot_sync(FULL, valid && op == 6u);
                 const uint32_t nstop = __ballot_sync(FULL, valid && !(e & 8u));
-                uint32_t val = pv;
+                if (!final_level && valid && c == 0) cmask[q] = (uint8_t)(nstop >> (lane & 24));
+                if (!valid) continue;
+                const uint32_t j = (q << 3) | c;
+                uint32_t val;
                 int st = 0;
                 bool chain = false;
-                const uint32_t j = (q << 3) | c;
-                if (op >= 1 && op <= 3) {
-                    const int a = op - 1;
-                    const uint32_t M = axis_mask(a, cbits);
+                if (op - 1u < 3u) {
+                    const uint32_t a = op - 1u;
+                    const uint32_t M = a == 0 ? Mx : (a == 1 ? My : Mz);
                     const uint32_t part = j & M;
-                    if ((c >> a) & 1) {      // odd: the +1 neighbour is decoded later -> its parent's value
-                        if (part == M) st = CSV_ST_BAD_NEIGHBOR;
-                        else val = plev[((((part | ~M) + 1u) & M) | (j & ~M)) >> 3];
-                    } else {                 // even: the -1 neighbour at this level (resolved in rounds)
-                        if (part == 0) st = CSV_ST_BAD_NEIGHBOR;
-                        else chain = true;
+                    if ((c >> a) & 1u) {   // odd: the +1 neighbour is decoded later -> its parent's value
+                        st = part == M ? CSV_ST_BAD_NEIGHBOR : 0;
+                        val = plev[((((part | ~M) + 1u) & M) | (j & ~M)) >> 3];
+                    } else {               // even: the -1 neighbour at this level (resolved in rounds)
+                        st = part == 0 ? CSV_ST_BAD_NEIGHBOR : 0;
+                        chain = st == 0;
+                        val = 0;
                     }
-                } else if (op >= 4 && op <= 6) {
-                    const int64_t ip = ipbase + (int64_t)ipb[valid ? rk : 0] + __popc(pam & seg & ((1u << lane) - 1u));
-                    int64_t idx;
-                    if (op == 4) idx = ip;
-                    else if (op == 5) { idx = ip - (int64_t)(e >> 4) - 1; if (idx < 0) st = CSV_ST_DELTA_RANGE; }
-                    else { idx = ip + 1; if (idx >= (int64_t)plen) st = CSV_ST_PALETTE_RANGE; }
-                    idx = idx < 0 ? 0 : (idx >= (int64_t)plen ? (int64_t)plen - 1 : idx);
+                } else if (op - 4u < 3u) {
+                    const int32_t ip = ipbase + (int32_t)ipb[rk] + __popc(pam & (0xFFu << (lane & 24)) & ((1u << lane) - 1u));
+                    int32_t idx = op == 4u ? ip : (op == 5u ? ip - (int32_t)(e >> 4) - 1 : ip + 1);
+                    st = idx < 0 ? CSV_ST_DELTA_RANGE : (idx >= (int32_t)plen ? CSV_ST_PALETTE_RANGE : 0);
+                    idx = min(max(idx, 0), (int32_t)plen - 1);
                     val = __ldg(pal + idx);
+                } else {
+                    val = plev[q];
                 }
-                if (valid && ent < nvalid) {
-                    unsigned long long kk = ~0ull;
-                    if (op == 7) kk = ekey(ent, 0, CSV_ST_BAD_OP);
-                    else if (leaf && (e & 8u)) kk = ekey(ent, 1, CSV_ST_LEAF_STOP);
-                    else if (st) kk = ekey(ent, 2, st);
-                    myerr = kk < myerr ? kk : myerr;
+                if (ent < nvalid && (op == 7u || (leaf && (e & 8u)) || st)) {
+                    const unsigned long long kk = op == 7u ? ekey(ent, 0, CSV_ST_BAD_OP)
+                                                           : (leaf && (e & 8u)) ? ekey(ent, 1, CSV_ST_LEAF_STOP)
+                                                                                 : ekey(ent, 2, st);
+                    atomicMin(&S.errkey, kk);
                 }
-                if (!final_level && valid && c == 0)
-                    reinterpret_cast<uint8_t*>(cmask)[q] = (uint8_t)(nstop >> (lane & 24));
-                if (valid) {
-                    if (chain) {
-                        atomicOr(&pend[j >> 5], 1u << (j & 31));
-                    } else {
-                        uint32_t* slot = child_slot<MODE>(final_level, clev, out_m, R, P, j);
-                        if (slot) *slot = val;
-                    }
+                if (chain) {
+                    atomicOr(&pend[j >> 5], 1u << (j & 31));
+                } else {
+                    uint32_t* slot = !final_level ? clev + j
+                                     : (MODE == OUT_MORTON ? out_m + j : raster_slot(R, P, S, j));
+                    if (slot) *slot = val;
                 }
             }
-            if (myerr != ~0ull) atomicMin(&S.errkey, myerr);
             // (C2) inactive parents: their children repeat the parent value
-            if (final_level && MODE == OUT_RASTER) {
-                const int pb = N - l;
-                const uint32_t pm = (1u << pb) - 1u;
-                for (uint32_t i = threadIdx.x; i < Pn; i += blockDim.x) {
-                    const uint32_t qx = i & pm, qy = (i >> pb) & pm, qz = i >> (2 * pb);
-                    const uint32_t q = spread3_u32(qx) | (spread3_u32(qy) << 1) | (spread3_u32(qz) << 2);
-                    if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
-                    const uint32_t pv = plev[q];
-#pragma unroll
-                    for (int row = 0; row < 4; ++row)
-                        store_pair(R, P, 2 * qx, 2 * qy + (row & 1), 2 * qz + (row >> 1), pv, pv);
-                }
-            } else {
-                for (uint32_t q = threadIdx.x; q < Pn; q += blockDim.x) {
-                    if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
-                    const uint32_t pv = plev[q];
-                    uint32_t* dstp = final_level ? out_m + 8ull * q : clev + 8 * q;
-                    if (!final_level || ((reinterpret_cast<uintptr_t>(dstp) & 15) == 0)) {
-                        reinterpret_cast<uint4*>(dstp)[0] = make_uint4(pv, pv, pv, pv);
-                        reinterpret_cast<uint4*>(dstp)[1] = make_uint4(pv, pv, pv, pv);
+            for (uint32_t q = threadIdx.x; q < Pn; q += blockDim.x) {
+                if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
+                const uint32_t pv = plev[q];
+                if (!final_level) {
+                    reinterpret_cast<uint4*>(clev + 8 * q)[0] = make_uint4(pv, pv, pv, pv);
+                    reinterpret_cast<uint4*>(clev + 8 * q)[1] = make_uint4(pv, pv, pv, pv);
+                    cmask[q] = 0;
+                } else if (MODE == OUT_MORTON) {
+                    uint32_t* d = out_m + 8ull * q;
+                    if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+                        reinterpret_cast<uint4*>(d)[0] = make_uint4(pv, pv, pv, pv);
+                        reinterpret_cast<uint4*>(d)[1] = make_uint4(pv, pv, pv, pv);
                     } else {
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) dstp[c] = pv;
+                        for (int c = 0; c < 8; ++c) d[c] = pv;
                     }
-                    if (!final_level) reinterpret_cast<uint8_t*>(cmask)[q] = 0;
+                } else if (R.fast) {
+                    const uint32_t o = S.lut_lo[(8 * q) & 511] + S.lut_hi[(8 * q) >> 9];
+                    const uint32_t cxp = S.lut_lo[2], plane = S.lut_lo[4];
+                    uint32_t* d = R.base + o;
+                    if ((reinterpret_cast<uintptr_t>(d) & 7) == 0 && (cxp & 1) == 0) {
+                        const uint2 v2 = make_uint2(pv, pv);
+                        *reinterpret_cast<uint2*>(d) = v2;
+                        *reinterpret_cast<uint2*>(d + cxp) = v2;
+                        *reinterpret_cast<uint2*>(d + plane) = v2;
+                        *reinterpret_cast<uint2*>(d + plane + cxp) = v2;
+                    } else {
+                        d[0] = pv; d[1] = pv; d[cxp] = pv; d[cxp + 1] = pv;
+                        d[plane] = pv; d[plane + 1] = pv; d[plane + cxp] = pv; d[plane + cxp + 1] = pv;
+                    }
+                } else {
+#pragma unroll
+                    for (uint32_t c = 0; c < 8; ++c) {
+                        uint32_t* p = raster_slot(R, P, S, 8 * q + c);
+                        if (p) *p = pv;
+                    }
                 }
             }
             if (threadIdx.x == 0 && (uint64_t)e0 + 8ull * nact > nvalid)
@@ -733,17 +722,17 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
                         bits &= bits - 1;
                         const uint32_t j = 32 * wdx + bit;
                         const uint32_t q = j >> 3;
-                        const int c = j & 7;
                         const uint32_t rk = wpre[q >> 5] + __popc(pmask[q >> 5] & ((1u << (q & 31)) - 1u));
-                        const uint32_t e = __ldg(Eb + e0 + 8 * rk + c);
-                        const int a = (int)(e & 7u) - 1;
-                        const uint32_t M = axis_mask(a, cbits);
+                        const uint32_t a = (__ldg(Eb + e0 + 8 * rk + (j & 7)) & 7u) - 1u;
+                        const uint32_t M = a == 0 ? Mx : (a == 1 ? My : Mz);
                         const uint32_t nm = (((j & M) - 1u) & M) | (j & ~M);
                         if ((*(volatile uint32_t*)&pend[nm >> 5] >> (nm & 31)) & 1u) { any = 1; continue; }
                         __threadfence_block();
-                        uint32_t* dst = child_slot<MODE>(final_level, clev, out_m, R, P, j);
+                        uint32_t* dst = !final_level ? clev + j
+                                        : (MODE == OUT_MORTON ? out_m + j : raster_slot(R, P, S, j));
                         if (dst) {
-                            const uint32_t* srcp = child_slot<MODE>(final_level, clev, out_m, R, P, nm);
+                            const uint32_t* srcp = !final_level ? clev + nm
+                                                   : (MODE == OUT_MORTON ? out_m + nm : raster_slot(R, P, S, nm));
                             *(volatile uint32_t*)dst = *(volatile const uint32_t*)srcp;
                         }
                         __threadfence_block();
@@ -753,7 +742,7 @@ k2_replay(VolView V, Plan P, int Lmax, uint32_t* gws, uint64_t ws_stride) {
                 if (!__syncthreads_or(any)) break;
             }
             if (leaf) cur_d = e0 + 8 * nact; else cur_c = e0 + 8 * nact;
-            ipbase += tot_pa;
+            ipbase += (int32_t)tot_pa;
             cur ^= 1;
         }
         if (!failed) {
@@ -824,6 +813,26 @@ size_t k2_smem_bytes(int L) { return (size_t)make_layout(L, 2).words * 4; }
 uint64_t k2_gws_words(int L) { return make_layout(L, 4).words; }
 
 // Decode a plan: sizes -> scan -> K1 -> K2.  Workspace pointers are provided by the caller.
+template <int MODE, int L>
+static void k2_launch_one(unsigned grid, size_t smem, const VolView& V, const Plan& P, cudaStream_t st) {
+    cudaFuncSetAttribute(k2_replay<MODE, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k2_replay<MODE, L><<<grid, K2_THREADS, smem, st>>>(V, P, nullptr, 0);
+}
+template <int MODE>
+static void k2_launch_mode(int L, unsigned grid, size_t smem, const VolView& V, const Plan& P, cudaStream_t st) {
+    switch (L) {
+        case 1: k2_launch_one<MODE, 1>(grid, smem, V, P, st); break;
+        case 2: k2_launch_one<MODE, 2>(grid, smem, V, P, st); break;
+        case 3: k2_launch_one<MODE, 3>(grid, smem, V, P, st); break;
+        case 4: k2_launch_one<MODE, 4>(grid, smem, V, P, st); break;
+        default: k2_launch_one<MODE, 5>(grid, smem, V, P, st); break;
+    }
+}
+static void launch_k2_smem(int mode, int L, unsigned grid, size_t smem, const VolView& V, const Plan& P, cudaStream_t st) {
+    if (mode == OUT_RASTER) k2_launch_mode<OUT_RASTER>(L, grid, smem, V, P, st);
+    else k2_launch_mode<OUT_MORTON>(L, grid, smem, V, P, st);
+}
+
 cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                        unsigned long long* counter, uint32_t* gws, uint64_t gws_stride, int gws_ctas,
                        int nsm, int min_t, cudaStream_t st, cudaEvent_t* ev) {
@@ -838,24 +847,22 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
     if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
     else launch_k1<false>(V, P, counter, nsm, st);
     if (ev) cudaEventRecord(ev[2], st);
-    // K2 smem variant (N - t <= 5)
+    // K2: shared-memory instantiation for N - t <= 5, global workspace above
     int Ls = V.N - min_t;
     if (Ls > 5) Ls = 5;
     if (Ls < 1) Ls = 1;
     size_t smem = k2_smem_bytes(Ls);
     unsigned grid = (unsigned)(P.n < 0x7fffffffull ? P.n : 0x7fffffffull);
-    if (mode == OUT_RASTER) {
-        cudaFuncSetAttribute(k2_replay<OUT_RASTER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k2_replay<OUT_RASTER, true><<<grid, K2_THREADS, smem, st>>>(V, P, Ls, nullptr, 0);
-    } else {
-        cudaFuncSetAttribute(k2_replay<OUT_MORTON, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k2_replay<OUT_MORTON, true><<<grid, K2_THREADS, smem, st>>>(V, P, Ls, nullptr, 0);
-    }
+    launch_k2_smem(mode, Ls, grid, smem, V, P, st);
     if (V.N - min_t > 5 && gws) {
         unsigned g = (unsigned)(P.n < (uint64_t)gws_ctas ? P.n : (uint64_t)gws_ctas);
-        int Lg = V.N - min_t;
-        if (mode == OUT_RASTER) k2_replay<OUT_RASTER, false><<<g, K2_THREADS, 0, st>>>(V, P, Lg, gws, gws_stride);
-        else k2_replay<OUT_MORTON, false><<<g, K2_THREADS, 0, st>>>(V, P, Lg, gws, gws_stride);
+        if (V.N - min_t == 6) {
+            if (mode == OUT_RASTER) k2_replay<OUT_RASTER, 6><<<g, K2_THREADS, 0, st>>>(V, P, gws, gws_stride);
+            else k2_replay<OUT_MORTON, 6><<<g, K2_THREADS, 0, st>>>(V, P, gws, gws_stride);
+        } else {
+            if (mode == OUT_RASTER) k2_replay<OUT_RASTER, 7><<<g, K2_THREADS, 0, st>>>(V, P, gws, gws_stride);
+            else k2_replay<OUT_MORTON, 7><<<g, K2_THREADS, 0, st>>>(V, P, gws, gws_stride);
+        }
     }
     if (ev) cudaEventRecord(ev[3], st);
     return cudaGetLastError();
