@@ -325,7 +325,9 @@ __global__ void __launch_bounds__(K1_THREADS) k1_streams(VolView V, Plan P, unsi
 //   wpre : W+1 words, exclusive popcount prefix of the parent mask
 //   ipb  : per active parent (by rank) palette-advance prefix, level-relative
 //   list : per active parent (by rank) its Morton index
-//   pend : one bit per child of the level: "same-level chain not resolved yet"
+//   pend : one bit per child of the level (or final tile): "chain, value pending"
+//   pax  : two bits per child: the chain's axis
+//   buf  : final-level tile of 4096 children (16^3 voxels) staged before the HBM write
 // LMAX <= 5 lives in shared memory with 16-bit ipb/list (<= 4096 parents and
 // <= 32768 entries per level); LMAX 6, 7 (b = 64, 128 at fine LODs) use a
 // per-CTA global workspace with 32-bit indices.
@@ -333,12 +335,14 @@ __host__ __device__ constexpr uint32_t levoffA(int j) {
     return j == 0 ? 0u : 4u + ((1u << (3 * j)) - 8u) / 7u;
 }
 struct Layout {
-    uint32_t lev, mask, wpre, ipb, list, pend, words, W;   // offsets in u32 units
+    uint32_t lev, mask, wpre, ipb, list, pend, pax, buf, words, W;   // offsets in u32 units
 };
 __host__ __device__ constexpr Layout make_layout(int L, int idx_bytes) {
     Layout Y{};
     uint32_t nlev = levoffA(L);
-    uint32_t maxP = 1u << (3 * (L - 1));
+    uint32_t maxP = 1u << (3 * (L - 1));              // parents at level t+1 (= children of level t+2)
+    uint32_t ts = L >= 4 ? 4096u : (1u << (3 * L));   // final-level tile (children)
+    uint32_t pbits = maxP > ts ? maxP : ts;
     Y.W = (maxP + 31) / 32;
     Y.lev = 0;
     Y.mask = (nlev + 3) & ~3u;
@@ -347,7 +351,9 @@ __host__ __device__ constexpr Layout make_layout(int L, int idx_bytes) {
     uint32_t idx_words = (maxP * idx_bytes + 15) / 16 * 4;
     Y.list = Y.ipb + idx_words;
     Y.pend = Y.list + idx_words;
-    Y.words = Y.pend + (8 * maxP + 31) / 32;
+    Y.pax = Y.pend + (pbits + 31) / 32;
+    Y.buf = (Y.pax + (pbits + 15) / 16 + 3) & ~3u;
+    Y.words = Y.buf + ts;
     return Y;
 }
 
@@ -364,8 +370,6 @@ struct K2Shared {
     unsigned long long errkey;
     uint32_t scan[K2_WARPS + 1];
     uint64_t red64[2][K2_WARPS];
-    uint32_t lut_lo[512];    // raster offset of the low 3 Morton bit-triples (x + y*cx + z*plane)
-    uint32_t lut_hi[64];     // ... of the next 2 triples (scaled by 8)
 };
 
 // Block-wide in-place exclusive scan of arr[0..n); returns the total.
@@ -425,13 +429,6 @@ struct Raster {
     bool fast;
 };
 
-__device__ __forceinline__ uint32_t* raster_slot(const Raster& R, const Plan& P, const K2Shared& S, uint32_t j) {
-    if (R.fast) return R.base + (S.lut_lo[j & 511] + S.lut_hi[j >> 9]);
-    int64_t gx = R.ox + compact3(j), gy = R.oy + compact3(j >> 1), gz = R.oz + compact3(j >> 2);
-    if (gz < P.z_begin || gz >= P.z_end || gy >= P.cy || gx >= P.cx) return nullptr;
-    return P.out + ((gz - P.z_begin) * P.cy + gy) * P.cx + gx;
-}
-
 __device__ __forceinline__ void write_result(const Plan& P, uint64_t r, int st, int stream, int64_t pos,
                                              int64_t ci, int64_t di) {
     if (P.res && threadIdx.x == 0) {
@@ -441,22 +438,73 @@ __device__ __forceinline__ void write_result(const Plan& P, uint64_t r, int st, 
     }
 }
 
-// Fill the whole output of request r with one value (relevant == 0, codec.py:353-358).
-template <int MODE>
-__device__ void fill_output(int lb, const Plan& P, const Raster& R, const K2Shared& S, uint32_t* out_m, uint32_t val) {
-    const uint32_t n = 1u << (3 * lb);
-    if (MODE == OUT_MORTON) {
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out_m[i] = val;
-    } else {
-        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
-            uint32_t* p = raster_slot(R, P, S, j);
-            if (p) *p = val;
+// Evaluation of one child (lane-per-child; 8 consecutive lanes = one parent).
+// Returns the value for every op whose source is already final; sets *chain
+// for an even-coordinate reuse whose -1 neighbour has an active parent (its
+// value is produced at this level, codec.py:422-423) and reports that
+// neighbour in *nm_out.  Op-specific errors go to *st.
+struct ChildCtx {
+    const uint32_t* plev;
+    const uint32_t* pmask;
+    const uint32_t* pal;
+    uint32_t plen;
+    int32_t ipbase;
+    uint32_t Mx, My, Mz;
+};
+
+__device__ __forceinline__ uint32_t eval_child(const ChildCtx& C, uint32_t q, uint32_t c, uint32_t e, int32_t ipq,
+                                               uint32_t pam, int lane, int* st, bool* chain, uint32_t* nm_out,
+                                               uint32_t* axis) {
+    const uint32_t op = e & 7u;
+    const uint32_t j = (q << 3) | c;
+    *st = 0;
+    *chain = false;
+    if (op - 1u < 3u) {
+        const uint32_t a = op - 1u;
+        const uint32_t M = a == 0 ? C.Mx : (a == 1 ? C.My : C.Mz);
+        const uint32_t part = j & M;
+        *axis = a;
+        if ((c >> a) & 1u) {   // odd: the +1 neighbour is decoded later -> its parent's value
+            *st = part == M ? CSV_ST_BAD_NEIGHBOR : 0;
+            return C.plev[((((part | ~M) + 1u) & M) | (j & ~M)) >> 3];
         }
+        *st = part == 0 ? CSV_ST_BAD_NEIGHBOR : 0;    // even: the -1 neighbour, same level
+        const uint32_t nm = ((part - 1u) & M) | (j & ~M);
+        const uint32_t qn = nm >> 3;
+        *nm_out = nm;
+        *chain = *st == 0 && ((C.pmask[qn >> 5] >> (qn & 31)) & 1u);
+        return C.plev[qn];                                  // final when that parent is inactive
+    }
+    if (op - 4u < 3u) {
+        const int32_t ip = ipq + __popc(pam & (0xFFu << (lane & 24)) & ((1u << lane) - 1u));
+        int32_t idx = op == 4u ? ip : (op == 5u ? ip - (int32_t)(e >> 4) - 1 : ip + 1);
+        *st = idx < 0 ? CSV_ST_DELTA_RANGE : (idx >= (int32_t)C.plen ? CSV_ST_PALETTE_RANGE : 0);
+        idx = min(max(idx, 0), (int32_t)C.plen - 1);
+        return __ldg(C.pal + idx);
+    }
+    return C.plev[q];
+}
+
+__device__ __forceinline__ void record_error(K2Shared& S, uint32_t ent, uint32_t nvalid, uint32_t e, bool leaf, int st) {
+    const uint32_t op = e & 7u;
+    if (ent < nvalid && (op == 7u || (leaf && (e & 8u)) || st)) {
+        const unsigned long long kk = op == 7u ? ekey(ent, 0, CSV_ST_BAD_OP)
+                                               : (leaf && (e & 8u)) ? ekey(ent, 1, CSV_ST_LEAF_STOP) : ekey(ent, 2, st);
+        atomicMin(&S.errkey, kk);
     }
 }
 
+// Raster address of final-level child j (brick-local Morton at LOD t); nullptr if cropped.
+__device__ __forceinline__ uint32_t* raster_of(const Raster& R, const Plan& P, uint32_t j) {
+    const uint32_t x = compact3(j), y = compact3(j >> 1), z = compact3(j >> 2);
+    if (R.fast) return R.base + ((uint32_t)z * (uint32_t)(P.cx * P.cy) + (uint32_t)y * (uint32_t)P.cx + x);
+    const int64_t gx = R.ox + x, gy = R.oy + y, gz = R.oz + z;
+    if (gz < P.z_begin || gz >= P.z_end || gy >= P.cy || gx >= P.cx) return nullptr;
+    return P.out + ((gz - P.z_begin) * P.cy + gy) * P.cx + gx;
+}
+
 template <int MODE, int LMAX>
-__global__ void __launch_bounds__(K2_THREADS, LMAX <= 5 ? 5 : 1)
+__global__ void __launch_bounds__(K2_THREADS, LMAX <= 5 ? 4 : 1)
 k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
     constexpr bool SMEM = LMAX <= 5;
     using IdxT = typename std::conditional<SMEM, uint16_t, uint32_t>::type;
@@ -472,19 +520,11 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
     IdxT* const ipb = reinterpret_cast<IdxT*>(ws + Y.ipb);
     IdxT* const list = reinterpret_cast<IdxT*>(ws + Y.list);
     uint32_t* const pend = ws + Y.pend;
+    uint32_t* const pax = ws + Y.pax;
+    uint32_t* const buf = ws + Y.buf;
     const int N = V.N;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    if (MODE == OUT_RASTER) {
-        // Morton -> raster offset tables for this launch's pitches
-        const uint32_t cx = (uint32_t)P.cx, plane = (uint32_t)(P.cx * P.cy);
-        for (uint32_t m = threadIdx.x; m < 512 + 64; m += blockDim.x) {
-            uint32_t mm = m < 512 ? m : m - 512, sc = m < 512 ? 1u : 8u;
-            uint32_t off = sc * (compact3(mm) + compact3(mm >> 1) * cx + compact3(mm >> 2) * plane);
-            if (m < 512) S.lut_lo[mm] = off; else S.lut_hi[mm] = off;
-        }
-        __syncthreads();
-    }
     for (uint64_t r = blockIdx.x; r < P.n; r += gridDim.x) {
         const uint64_t b = req_local(V, P, r);
         const int t = req_lod(P, r);
@@ -502,12 +542,15 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
             R.oy = (int64_t)((gb / V.gx) % V.gy) * side;
             R.oz = (int64_t)(gb / (V.gx * V.gy)) * side;
             R.base = P.out + ((R.oz - P.z_begin) * P.cy + R.oy) * P.cx + R.ox;
-            R.fast = N - t <= 5 && R.ox + side <= P.cx && R.oy + side <= P.cy && R.oz >= P.z_begin &&
-                     R.oz + side <= P.z_end && (uint64_t)P.cx * P.cy * side < (1ull << 32);
+            R.fast = R.ox + side <= P.cx && R.oy + side <= P.cy && R.oz >= P.z_begin && R.oz + side <= P.z_end &&
+                     (uint64_t)P.cx * P.cy * side < (1ull << 32);
         }
         if (plen == 0) { write_result(P, r, CSV_ST_EMPTY_PALETTE, 0, 0, 0, 0); continue; }
         if (t == N) {   // coarsest LOD: palette[0] (codec.py:514-516, container.py:178-182)
-            fill_output<MODE>(0, P, R, S, out_m, __ldg(pal));
+            if (threadIdx.x == 0) {
+                uint32_t* p = MODE == OUT_MORTON ? out_m : raster_of(R, P, 0);
+                if (p) *p = __ldg(pal);
+            }
             write_result(P, r, 0, 0, 0, 0, 0);
             continue;
         }
@@ -517,16 +560,12 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
             if (nc_raw > 0 && V.c_bytes[b] < 4) { write_result(P, r, CSV_ST_UNDERRUN, 0, 0, 0, 0); continue; }
             if (t == 0 && nd_raw > 0 && V.d_bytes[b] < 4) { write_result(P, r, CSV_ST_UNDERRUN, 1, 0, 0, 0); continue; }
         }
-        if ((uint64_t)nc + nd == 0) {
-            fill_output<MODE>(N - t, P, R, S, out_m, __ldg(pal));
-            write_result(P, r, 0, 0, 0, 0, 0);
-            continue;
-        }
         const csv_stream_result src = P.sres[2 * r], srd = P.sres[2 * r + 1];
         const uint64_t eo0 = P.eoff[2 * r], eo1 = P.eoff[2 * r + 1], eo2 = P.eoff[2 * r + 2];
+        const bool trivial = (uint64_t)nc + nd == 0;     // relevant == 0: fill palette[0] (codec.py:353-358)
         if (threadIdx.x == 0) {
             lev[0] = __ldg(pal);      // root (codec.py:353)
-            mask0[0] = 1u;
+            mask0[0] = trivial ? 0u : 1u;
             S.errkey = ~0ull;
         }
         __syncthreads();
@@ -540,25 +579,28 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
             const bool final_level = (l - 1 == t);
             const uint32_t Pn = 1u << (3 * (N - l));
             const uint32_t W = (Pn + 31) >> 5;
-            const uint32_t PW = (8 * Pn + 31) >> 5;      // pending words (children)
             uint32_t* const pmask = mask0 + cur * Y.W;
             uint8_t* const cmask = reinterpret_cast<uint8_t*>(mask0 + (cur ^ 1) * Y.W);
             const csv_stream_result sr = leaf ? srd : src;
             const uint32_t e0 = leaf ? cur_d : cur_c;
             const uint8_t* const Eb = P.entries + (leaf ? eo1 : eo0);   // this stream's entry bytes
             const uint32_t ecap = (uint32_t)((leaf ? eo2 : eo1) - (leaf ? eo1 : eo0));
-            const uint32_t* const plev = lev + levoffA(N - l);
             uint32_t* const clev = lev + levoffA(N - l + 1);
             const int cbits = N - l + 1;
-            const uint32_t Mx = axis_mask(0, cbits), My = axis_mask(1, cbits), Mz = axis_mask(2, cbits);
-            // (A) rank prefix of active parents; clear pending bits
+            ChildCtx C;
+            C.plev = lev + levoffA(N - l);
+            C.pmask = pmask;
+            C.pal = pal;
+            C.plen = plen;
+            C.ipbase = ipbase;
+            C.Mx = axis_mask(0, cbits); C.My = axis_mask(1, cbits); C.Mz = axis_mask(2, cbits);
+            // (A) rank prefix of active parents
             for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
                 uint32_t mw = pmask[i];
                 if (Pn < 32) mw &= (1u << Pn) - 1u;
                 pmask[i] = mw;
                 wpre[i] = __popc(mw);
             }
-            for (uint32_t i = threadIdx.x; i < PW; i += blockDim.x) pend[i] = 0;
             __syncthreads();
             const uint32_t nact = block_scan_inplace(wpre, W, S);
             // (B) active list + palette-advance counts per active parent
@@ -581,102 +623,126 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
             __syncthreads();
             const uint32_t tot_pa = block_scan_inplace(ipb, nact, S);
             const uint32_t nvalid = sr.n_entries;
-            // (C1) one lane per child of an active parent (8 consecutive lanes = one parent)
-            const uint32_t nch = 8 * nact;
-            for (uint32_t kb = threadIdx.x - lane; kb < nch; kb += blockDim.x) {
-                const uint32_t k = kb + lane;
-                const bool valid = k < nch;
-                const uint32_t rk = k >> 3;
-                const uint32_t c = k & 7;
-                const uint32_t q = valid ? (uint32_t)list[rk] : 0u;
-                const uint32_t ent = e0 + k;
-                const uint32_t e = (valid && ent < ecap) ? (uint32_t)__ldg(Eb + ent) : 0u;
-                const uint32_t op = e & 7u;
-                const uint32_t pam = __ballot_sync(FULL, valid && op == 6u);
-                const uint32_t nstop = __ballot_sync(FULL, valid && !(e & 8u));
-                if (!final_level && valid && c == 0) cmask[q] = (uint8_t)(nstop >> (lane & 24));
-                if (!valid) continue;
-                const uint32_t j = (q << 3) | c;
-                uint32_t val;
-                int st = 0;
-                bool chain = false;
-                if (op - 1u < 3u) {
-                    const uint32_t a = op - 1u;
-                    const uint32_t M = a == 0 ? Mx : (a == 1 ? My : Mz);
-                    const uint32_t part = j & M;
-                    if ((c >> a) & 1u) {   // odd: the +1 neighbour is decoded later -> its parent's value
-                        st = part == M ? CSV_ST_BAD_NEIGHBOR : 0;
-                        val = plev[((((part | ~M) + 1u) & M) | (j & ~M)) >> 3];
-                    } else {               // even: the -1 neighbour at this level (resolved in rounds)
-                        st = part == 0 ? CSV_ST_BAD_NEIGHBOR : 0;
-                        chain = st == 0;
-                        val = 0;
-                    }
-                } else if (op - 4u < 3u) {
-                    const int32_t ip = ipbase + (int32_t)ipb[rk] + __popc(pam & (0xFFu << (lane & 24)) & ((1u << lane) - 1u));
-                    int32_t idx = op == 4u ? ip : (op == 5u ? ip - (int32_t)(e >> 4) - 1 : ip + 1);
-                    st = idx < 0 ? CSV_ST_DELTA_RANGE : (idx >= (int32_t)plen ? CSV_ST_PALETTE_RANGE : 0);
-                    idx = min(max(idx, 0), (int32_t)plen - 1);
-                    val = __ldg(pal + idx);
-                } else {
-                    val = plev[q];
-                }
-                if (ent < nvalid && (op == 7u || (leaf && (e & 8u)) || st)) {
-                    const unsigned long long kk = op == 7u ? ekey(ent, 0, CSV_ST_BAD_OP)
-                                                           : (leaf && (e & 8u)) ? ekey(ent, 1, CSV_ST_LEAF_STOP)
-                                                                                 : ekey(ent, 2, st);
-                    atomicMin(&S.errkey, kk);
-                }
-                if (chain) {
-                    atomicOr(&pend[j >> 5], 1u << (j & 31));
-                } else {
-                    uint32_t* slot = !final_level ? clev + j
-                                     : (MODE == OUT_MORTON ? out_m + j : raster_slot(R, P, S, j));
-                    if (slot) *slot = val;
-                }
-            }
-            // (C2) inactive parents: their children repeat the parent value
-            for (uint32_t q = threadIdx.x; q < Pn; q += blockDim.x) {
-                if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
-                const uint32_t pv = plev[q];
-                if (!final_level) {
-                    reinterpret_cast<uint4*>(clev + 8 * q)[0] = make_uint4(pv, pv, pv, pv);
-                    reinterpret_cast<uint4*>(clev + 8 * q)[1] = make_uint4(pv, pv, pv, pv);
-                    cmask[q] = 0;
-                } else if (MODE == OUT_MORTON) {
-                    uint32_t* d = out_m + 8ull * q;
-                    if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
-                        reinterpret_cast<uint4*>(d)[0] = make_uint4(pv, pv, pv, pv);
-                        reinterpret_cast<uint4*>(d)[1] = make_uint4(pv, pv, pv, pv);
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) d[c] = pv;
-                    }
-                } else if (R.fast) {
-                    const uint32_t o = S.lut_lo[(8 * q) & 511] + S.lut_hi[(8 * q) >> 9];
-                    const uint32_t cxp = S.lut_lo[2], plane = S.lut_lo[4];
-                    uint32_t* d = R.base + o;
-                    if ((reinterpret_cast<uintptr_t>(d) & 7) == 0 && (cxp & 1) == 0) {
-                        const uint2 v2 = make_uint2(pv, pv);
-                        *reinterpret_cast<uint2*>(d) = v2;
-                        *reinterpret_cast<uint2*>(d + cxp) = v2;
-                        *reinterpret_cast<uint2*>(d + plane) = v2;
-                        *reinterpret_cast<uint2*>(d + plane + cxp) = v2;
-                    } else {
-                        d[0] = pv; d[1] = pv; d[cxp] = pv; d[cxp + 1] = pv;
-                        d[plane] = pv; d[plane + 1] = pv; d[plane + cxp] = pv; d[plane + cxp + 1] = pv;
-                    }
-                } else {
-#pragma unroll
-                    for (uint32_t c = 0; c < 8; ++c) {
-                        uint32_t* p = raster_slot(R, P, S, 8 * q + c);
-                        if (p) *p = pv;
-                    }
-                }
-            }
             if (threadIdx.x == 0 && (uint64_t)e0 + 8ull * nact > nvalid)
                 atomicMin(&S.errkey, ekey(nvalid, 0, EK_UNDERRUN_NV));
-            __syncthreads();
+            // tiles: the whole child level for intermediate levels (shared level
+            // array), 4096-child Morton tiles staged in `buf` for the final level
+            const uint32_t Cn = 8 * Pn;
+            const uint32_t TS = final_level ? (Cn < 4096u ? Cn : 4096u) : Cn;
+            const uint32_t NT = Cn / TS;
+            const uint32_t PT = TS / 8;                   // parents per tile
+            for (uint32_t o = 0; o < NT; ++o) {
+                uint32_t* const dst = final_level ? buf : clev;
+                const uint32_t q0 = o * PT, q1 = q0 + PT;
+                const uint32_t j0 = 8 * q0;
+                const uint32_t r0 = wpre[q0 >> 5] + __popc(pmask[q0 >> 5] & ((1u << (q0 & 31)) - 1u));
+                const uint32_t r1 = q1 >= Pn ? nact : wpre[q1 >> 5] + __popc(pmask[q1 >> 5] & ((1u << (q1 & 31)) - 1u));
+                for (uint32_t i = threadIdx.x; i < TS / 32; i += blockDim.x) pend[i] = 0;
+                for (uint32_t i = threadIdx.x; i < TS / 16; i += blockDim.x) pax[i] = 0;
+                __syncthreads();
+                // (C1) children of active parents in this tile, one lane each
+                for (uint32_t kb = 8 * r0 + (threadIdx.x - lane); kb < 8 * r1; kb += blockDim.x) {
+                    const uint32_t k = kb + lane;
+                    const bool valid = k < 8 * r1;
+                    const uint32_t rk = k >> 3;
+                    const uint32_t c = k & 7;
+                    const uint32_t q = valid ? (uint32_t)list[rk] : q0;
+                    const uint32_t ent = e0 + k;
+                    const uint32_t e = (valid && ent < ecap) ? (uint32_t)__ldg(Eb + ent) : 0u;
+                    const uint32_t pam = __ballot_sync(FULL, valid && (e & 7u) == 6u);
+                    if (!final_level) {
+                        const uint32_t nstop = __ballot_sync(FULL, valid && !(e & 8u));
+                        if (valid && c == 0) cmask[q] = (uint8_t)(nstop >> (lane & 24));
+                    }
+                    if (!valid) continue;
+                    int st;
+                    bool chain;
+                    uint32_t nm = 0, a = 0;
+                    uint32_t val = eval_child(C, q, c, e, ipbase + (int32_t)ipb[rk], pam, lane, &st, &chain, &nm, &a);
+                    record_error(S, ent, nvalid, e, leaf, st);
+                    const uint32_t jl = ((q << 3) | c) - j0;
+                    if (chain && nm < j0) {       // neighbour in an earlier (already stored) tile
+                        chain = false;
+                        const uint32_t* p = MODE == OUT_MORTON ? out_m + nm : raster_of(R, P, nm);
+                        val = p ? *p : 0u;
+                    }
+                    if (chain) {
+                        atomicOr(&pend[jl >> 5], 1u << (jl & 31));
+                        atomicOr(&pax[jl >> 4], a << (2 * (jl & 15)));
+                    } else {
+                        dst[jl] = val;
+                    }
+                }
+                // (C2) inactive parents of this tile: children repeat the parent value
+                for (uint32_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+                    if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
+                    const uint32_t pv = C.plev[q];
+                    reinterpret_cast<uint4*>(dst + 8 * (q - q0))[0] = make_uint4(pv, pv, pv, pv);
+                    reinterpret_cast<uint4*>(dst + 8 * (q - q0))[1] = make_uint4(pv, pv, pv, pv);
+                    if (!final_level) cmask[q] = 0;
+                }
+                __syncthreads();
+                // (W) same-level chains: walk -1 neighbours (<= 3 hops: each hop makes
+                // one more coordinate odd) to the first child whose value is final
+                for (uint32_t w = threadIdx.x; w < TS / 32; w += blockDim.x) {
+                    uint32_t bits = pend[w];
+                    while (bits) {
+                        const uint32_t jl = 32 * w + (__ffs(bits) - 1);
+                        bits &= bits - 1;
+                        uint32_t cl = jl;
+                        for (int hop = 0; hop < 4; ++hop) {
+                            const uint32_t a = (pax[cl >> 4] >> (2 * (cl & 15))) & 3u;
+                            const uint32_t M = a == 0 ? C.Mx : (a == 1 ? C.My : C.Mz);
+                            const uint32_t jg = cl + j0;
+                            cl = ((((jg & M) - 1u) & M) | (jg & ~M)) - j0;
+                            if (!((pend[cl >> 5] >> (cl & 31)) & 1u)) break;
+                        }
+                        dst[jl] = dst[cl];
+                    }
+                }
+                __syncthreads();
+                if (!final_level) continue;
+                // (T) stream the tile to HBM: Morton pool (linear) or raster rows
+                if (MODE == OUT_MORTON) {
+                    uint32_t* d = out_m + (size_t)TS * o;
+                    const bool al = (reinterpret_cast<uintptr_t>(d) & 15) == 0;
+                    for (uint32_t i = threadIdx.x; i < TS / 4; i += blockDim.x) {
+                        const uint4 v = reinterpret_cast<const uint4*>(buf)[i];
+                        if (al) reinterpret_cast<uint4*>(d)[i] = v;
+                        else { d[4 * i] = v.x; d[4 * i + 1] = v.y; d[4 * i + 2] = v.z; d[4 * i + 3] = v.w; }
+                    }
+                } else {
+                    const int tb = (31 - __clz(TS)) / 3;          // log2 of the tile side
+                    const uint32_t ts = 1u << tb;
+                    const uint32_t tx = compact3(o) << tb, ty = compact3(o >> 1) << tb, tz = compact3(o >> 2) << tb;
+                    const uint32_t xs = ts >= 4 ? 4u : ts;         // voxels per item along x
+                    const uint32_t ipr = ts / xs;                   // items per row
+                    for (uint32_t i = threadIdx.x; i < TS / xs; i += blockDim.x) {
+                        const uint32_t x = (i % ipr) * xs, y = (i / ipr) % ts, z = i / (ipr * ts);
+                        const uint32_t myz = (spread3_u32(y) << 1) | (spread3_u32(z) << 2);
+                        uint32_t v[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) v[k] = k < (int)xs ? buf[myz | spread3_u32(x + k)] : 0u;
+                        if (R.fast) {
+                            uint32_t* p = R.base + ((tz + z) * (uint32_t)(P.cx * P.cy) + (ty + y) * (uint32_t)P.cx + tx + x);
+                            if (xs == 4 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+                                *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+                            } else {
+                                for (uint32_t k = 0; k < xs; ++k) p[k] = v[k];
+                            }
+                        } else {
+                            const int64_t gz = R.oz + tz + z, gy = R.oy + ty + y;
+                            if (gz < P.z_begin || gz >= P.z_end || gy >= P.cy) continue;
+                            uint32_t* row = P.out + ((gz - P.z_begin) * P.cy + gy) * P.cx;
+                            for (uint32_t k = 0; k < xs; ++k) {
+                                const int64_t gx = R.ox + tx + x + k;
+                                if (gx < P.cx) row[gx] = v[k];
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
             const unsigned long long ek = S.errkey;
             if (ek != ~0ull) {
                 // first failing entry in sequential order -> status + nibble position
@@ -709,37 +775,6 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
                 write_result(P, r, st, leaf ? 1 : 0, pos, 0, 0);
                 failed = true;
                 break;
-            }
-            // (R) same-level chains (codec.py:422-423, nm < j): a child copies its -1
-            // neighbour once that one is final.  Hops make coordinates odd, so a
-            // chain is at most 3 deep and resolves within 3 rounds.
-            for (int round = 0; round < 4; ++round) {
-                int any = 0;
-                for (uint32_t wdx = threadIdx.x; wdx < PW; wdx += blockDim.x) {
-                    uint32_t bits = *(volatile uint32_t*)&pend[wdx];
-                    while (bits) {
-                        const int bit = __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        const uint32_t j = 32 * wdx + bit;
-                        const uint32_t q = j >> 3;
-                        const uint32_t rk = wpre[q >> 5] + __popc(pmask[q >> 5] & ((1u << (q & 31)) - 1u));
-                        const uint32_t a = (__ldg(Eb + e0 + 8 * rk + (j & 7)) & 7u) - 1u;
-                        const uint32_t M = a == 0 ? Mx : (a == 1 ? My : Mz);
-                        const uint32_t nm = (((j & M) - 1u) & M) | (j & ~M);
-                        if ((*(volatile uint32_t*)&pend[nm >> 5] >> (nm & 31)) & 1u) { any = 1; continue; }
-                        __threadfence_block();
-                        uint32_t* dst = !final_level ? clev + j
-                                        : (MODE == OUT_MORTON ? out_m + j : raster_slot(R, P, S, j));
-                        if (dst) {
-                            const uint32_t* srcp = !final_level ? clev + nm
-                                                   : (MODE == OUT_MORTON ? out_m + nm : raster_slot(R, P, S, nm));
-                            *(volatile uint32_t*)dst = *(volatile const uint32_t*)srcp;
-                        }
-                        __threadfence_block();
-                        atomicAnd(&pend[j >> 5], ~(1u << (j & 31)));
-                    }
-                }
-                if (!__syncthreads_or(any)) break;
             }
             if (leaf) cur_d = e0 + 8 * nact; else cur_c = e0 + 8 * nact;
             ipbase += (int32_t)tot_pa;
