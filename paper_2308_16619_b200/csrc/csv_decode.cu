@@ -504,7 +504,10 @@ __device__ __forceinline__ uint32_t* raster_of(const Raster& R, const Plan& P, u
 }
 
 template <int MODE, int LMAX>
-__global__ void __launch_bounds__(K2_THREADS, LMAX <= 5 ? 4 : 1)
+#ifndef K2_MINB
+#define K2_MINB 4
+#endif
+__global__ void __launch_bounds__(K2_THREADS, LMAX <= 5 ? K2_MINB : 1)
 k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
     constexpr bool SMEM = LMAX <= 5;
     using IdxT = typename std::conditional<SMEM, uint16_t, uint32_t>::type;
@@ -796,6 +799,8 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
     }
 }
 
+#include "csv_replay_fast.cuh"
+
 // Coarsest-LOD raster (t == N): one voxel per brick.
 __global__ void k_root_raster(VolView V, Plan P) {
     uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -850,8 +855,8 @@ uint64_t k2_gws_words(int L) { return make_layout(L, 4).words; }
 // Decode a plan: sizes -> scan -> K1 -> K2.  Workspace pointers are provided by the caller.
 template <int MODE, int L>
 static void k2_launch_one(unsigned grid, size_t smem, const VolView& V, const Plan& P, cudaStream_t st) {
-    cudaFuncSetAttribute(k2_replay<MODE, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k2_replay<MODE, L><<<grid, K2_THREADS, smem, st>>>(V, P, nullptr, 0);
+    cudaFuncSetAttribute(k2_fast<MODE, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k2_fast<MODE, L><<<grid, K2_THREADS, smem, st>>>(V, P);
 }
 template <int MODE>
 static void k2_launch_mode(int L, unsigned grid, size_t smem, const VolView& V, const Plan& P, cudaStream_t st) {
