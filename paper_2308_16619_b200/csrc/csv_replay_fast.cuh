@@ -214,22 +214,48 @@ __global__ void __launch_bounds__(K2_THREADS, 4) k2_fast(VolView V, Plan P) {
                 if (!final_level) cmask[q] = 0;
             }
             __syncthreads();
-            // (W) chains: walk -1 neighbours to the first final value (<= 3 hops)
-            for (uint32_t w = threadIdx.x; w < TS / 32; w += K2_THREADS) {
-                uint32_t bits = dsm[Y.pend + w];
-                while (bits) {
-                    const uint32_t jl = 32 * w + (__ffs(bits) - 1);
-                    bits &= bits - 1;
-                    uint32_t cl = jl;
-#pragma unroll 1
-                    for (int hop = 0; hop < 4; ++hop) {
-                        const uint32_t aa = (dsm[Y.pax + (cl >> 4)] >> (2 * (cl & 15))) & 3u;
-                        const uint32_t MM = aa == 0 ? Mx : (aa == 1 ? My : Mz);
-                        const uint32_t jg = cl + j0;
-                        cl = ((((jg & MM) - 1u) & MM) | (jg & ~MM)) - j0;
-                        if (!((dsm[Y.pend + (cl >> 5)] >> (cl & 31)) & 1u)) break;
+            // (W) chains: walk -1 neighbours to the first final value (<= 3 hops).
+            // Each warp compacts the pending bits of its words (ballot-free scan
+            // over lanes) so that every lane walks one chain.
+            {
+                const uint32_t NWd = TS / 32;
+                const uint32_t wpw = (NWd + K2_WARPS - 1) / K2_WARPS;
+                const uint32_t wbeg = (threadIdx.x >> 5) * wpw, wend = min(wbeg + wpw, NWd);
+                for (uint32_t wb = wbeg; wb < wend; wb += 32) {
+                    const uint32_t wi = wb + lane;
+                    const uint32_t word = wi < wend ? dsm[Y.pend + wi] : 0u;
+                    const uint32_t cnt = __popc(word);
+                    uint32_t inc = cnt;
+#pragma unroll
+                    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o2);
+                        if (lane >= o2) inc += u;
                     }
-                    dsm[dst_off + jl] = dsm[dst_off + cl];
+                    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+                    const uint32_t excl = inc - cnt;
+                    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+                        const uint32_t sidx = k0 + lane;
+                        int src = 0;
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1) {
+                            const uint32_t ex = __shfl_sync(0xffffffffu, excl, src + step);
+                            if (src + step < 32 && ex <= sidx) src += step;
+                        }
+                        const uint32_t wsrc = __shfl_sync(0xffffffffu, word, src);
+                        const uint32_t esrc = __shfl_sync(0xffffffffu, excl, src);
+                        if (sidx >= total) continue;
+                        const uint32_t jl = 32 * (wb + src) + __fns(wsrc, 0, (int)(sidx - esrc) + 1);
+                        uint32_t cl = jl;
+#pragma unroll 1
+                        for (int hop = 0; hop < 4; ++hop) {
+                            const uint32_t aa = (dsm[Y.pax + (cl >> 4)] >> (2 * (cl & 15))) & 3u;
+                            const uint32_t MM = aa == 0 ? Mx : (aa == 1 ? My : Mz);
+                            const uint32_t jg = cl + j0;
+                            cl = ((((jg & MM) - 1u) & MM) | (jg & ~MM)) - j0;
+                            if (!((dsm[Y.pend + (cl >> 5)] >> (cl & 31)) & 1u)) break;
+                        }
+                        dsm[dst_off + jl] = dsm[dst_off + cl];
+                    }
                 }
             }
             __syncthreads();
