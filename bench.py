@@ -132,12 +132,6 @@ def dist_setup(args):
     return world, rank, local
 
 
-def bz_range(gz: int, world: int, rank: int):
-    base, extra = divmod(gz, world)
-    z0 = rank * base + min(rank, extra)
-    return z0, z0 + base + (1 if rank < extra else 0)
-
-
 def max_over_ranks(v: float, world: int) -> float:
     if world == 1:
         return v
@@ -223,6 +217,7 @@ def desired_lods(grid, b, cam, fov, height, max_lod):
 def run_ours(args, world, rank, local):
     import torch
     import paper_2308_16619_b200 as p
+    from paper_2308_16619_b200.distributed import bz_range
     wl = dict(WORKLOADS[args.workload])
     if args.zlayers:
         wl["dims"] = (wl["dims"][0], wl["dims"][1], 32 * args.zlayers)
