@@ -95,7 +95,8 @@ int csv_volume_create(int device, const uint8_t* head120, const uint8_t* dir44,
                       uintptr_t stream, csv_volume** vol);
 
 /* Same, from DEVICE memory already resident (e.g. the GPU encoder's output).
- * The blobs are borrowed (not copied): keep them alive until csv_volume_free. */
+  * The blobs are borrowed (not copied): keep them alive until csv_volume_free;
+ * each must have >= 64 readable bytes past its end (stream prefetch). */
 int csv_volume_create_device(int device, const uint8_t* head120, const uint8_t* d_dir44,
                              uint64_t brick_begin, uint64_t brick_end,
                              const uint32_t* d_palette, uint64_t palette_base, uint64_t palette_len,

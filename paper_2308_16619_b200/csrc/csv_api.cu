@@ -104,7 +104,7 @@ __global__ void k_unpack_dir(const uint8_t* dir44, uint64_t n, uint64_t pal_base
 __global__ void k_region_stats(VolView V, unsigned long long* total, unsigned long long* mx) {
     uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     unsigned long long s = 0;
-    if (b < V.nb && V.N > 0) s = round16(stream_limit(V, b, 0, 0)) + round16(stream_limit(V, b, 0, 1));
+    if (b < V.nb && V.N > 0) s = round32(stream_limit(V, b, 0, 0)) + round32(stream_limit(V, b, 0, 1));
     unsigned long long m = s;
     for (int o = 16; o > 0; o >>= 1) {
         s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -247,9 +247,9 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
         v->V.coarse = coarse;
         v->V.detail = detail;
     } else {
-        uint64_t pb = ((palette_len * 4 + 15) & ~15ull) + 16;
-        uint64_t cb = ((coarse_len + 15) & ~15ull) + 16;
-        uint64_t db = ((detail_len + 15) & ~15ull) + 16;
+        uint64_t pb = ((palette_len * 4 + 15) & ~15ull) + kBlobPad;
+        uint64_t cb = ((coarse_len + 15) & ~15ull) + kBlobPad;
+        uint64_t db = ((detail_len + 15) & ~15ull) + kBlobPad;
         ce = cudaMalloc(&v->d_blob, pb + cb + db);
         if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "blobs: %s", cudaGetErrorString(ce)); }
         cudaMemsetAsync(v->d_blob, 0, pb + cb + db, st);

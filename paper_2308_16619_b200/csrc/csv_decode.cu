@@ -40,7 +40,7 @@ __global__ void k_region_sizes(VolView V, Plan P, uint64_t* sizes) {
     uint64_t b = req_local(V, P, r);
     int t = req_lod(P, r);
     uint32_t lim = (b < V.nb && t < V.N) ? stream_limit(V, b, t, s) : 0;
-    sizes[i] = round16(lim);
+    sizes[i] = round32(lim);
 }
 
 // Simple 3-phase exclusive scan of u64 (n <= 4096 * 4096).
@@ -117,22 +117,24 @@ __global__ void k_scan_add(uint64_t* out, uint64_t n, const uint64_t* block_sums
 
 // ============================================================================ K1: entropy lanes
 // Per-lane stream state.  The byte reader keeps a 64-bit MSB-first bit buffer
-// (renorm bytes are consumed in stream order, rans.py:9-11) plus one aligned
-// 32-bit word in flight, so each refill's load latency overlaps ~6 symbols.
+// (renorm bytes are consumed in stream order, rans.py:9-11) fed from 16-byte
+// aligned chunks with one chunk in flight (~25 symbols of prefetch distance).
 struct Lane {
-    const uint32_t* wp;     // next aligned word to prefetch
+    const uint4* qp;        // next 16-byte chunk to prefetch
+    uint4 cq;               // current chunk (words consumed from .x, rotated)
+    uint4 nq;               // prefetched chunk
     uint64_t buf;           // upcoming stream bits, MSB first
-    uint64_t acc;           // pending entry bytes (<= 8)
-    uint64_t* outp;         // entry region (8-byte groups)
+    uint64_t acc;           // entry bytes of the group being built (<= 8)
+    uint64_t* outp;         // entry region (32-byte aligned)
     const uint8_t* rawp;    // raw mode: packed nibble bytes
-    uint32_t nxt;           // prefetched word
     uint32_t x;             // rANS state (fits 32 bits: f*(x>>12) < 2^32)
     uint32_t pos, len;      // bytes consumed (incl. 4 state bytes) / stream bytes
     uint32_t i, lim, n;     // nibble index, nibble limit, stored count
-    uint32_t g;             // groups stored
+    uint32_t g4;            // 8-entry groups stored
     uint32_t cur;           // current entry byte
     uint64_t item;
     int nb;                 // valid bits in buf
+    int cw;                 // words left in cq
     int k;                  // entries in acc
     int tsel;               // decode table (0 interior, 1 leaf)
     bool pend;              // next nibble is a P_delta payload
@@ -141,11 +143,22 @@ struct Lane {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
+__device__ __forceinline__ uint32_t lane_next_word(Lane& L) {
+    if (L.cw == 0) {
+        L.cq = L.nq;
+        L.nq = __ldg(L.qp);
+        ++L.qp;
+        L.cw = 4;
+    }
+    const uint32_t w = L.cq.x;
+    L.cq.x = L.cq.y; L.cq.y = L.cq.z; L.cq.z = L.cq.w;
+    --L.cw;
+    return w;
+}
+
 __device__ __forceinline__ void lane_refill(Lane& L) {
-    L.buf |= (uint64_t)bswap32(L.nxt) << (32 - L.nb);
+    L.buf |= (uint64_t)bswap32(lane_next_word(L)) << (32 - L.nb);
     L.nb += 32;
-    L.nxt = __ldg(L.wp);
-    ++L.wp;
 }
 
 __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
@@ -155,7 +168,7 @@ __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
     if (!L.pend) {
         L.acc |= (uint64_t)L.cur << (8 * L.k);
         if (++L.k == 8) {
-            L.outp[L.g++] = L.acc;
+            L.outp[L.g4++] = L.acc;
             L.acc = 0;
             L.k = 0;
         }
@@ -163,9 +176,9 @@ __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
 }
 
 __device__ __forceinline__ void lane_finish(Lane& L, const Plan& P, bool failed, bool entropy) {
-    if (L.k > 0) L.outp[L.g] = L.acc;
+    if (L.k > 0) L.outp[L.g4] = L.acc;
     csv_stream_result r;
-    r.n_entries = L.g * 8 + L.k;
+    r.n_entries = L.g4 * 8 + L.k;
     r.flags = 0;
     r.fail_nibble = 0xffffffffu;
     r.partial_op = 0;
@@ -191,7 +204,7 @@ __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t ite
     int s = item < P.n ? 1 : 0;           // detail streams first (longest chains)
     uint64_t w = 2 * r + s;               // result / region index
     L.item = w;
-    L.acc = 0; L.k = 0; L.g = 0; L.pend = false; L.cur = 0; L.i = 0; L.slow = false;
+    L.acc = 0; L.k = 0; L.g4 = 0; L.pend = false; L.cur = 0; L.i = 0; L.slow = false;
     L.x = 0; L.pos = 0; L.len = 0; L.nb = 0; L.buf = 0;
     uint64_t b = req_local(V, P, r);
     int t = req_lod(P, r);
@@ -223,13 +236,15 @@ __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t ite
     L.x = (uint32_t)base[0] | ((uint32_t)base[1] << 8) | ((uint32_t)base[2] << 16) | ((uint32_t)base[3] << 24);
     L.pos = 4;
     uintptr_t q = reinterpret_cast<uintptr_t>(base) + 4;
-    const uint32_t* aq = reinterpret_cast<const uint32_t*>(q & ~uintptr_t(3));
-    int sh = (int)(q & 3);
-    L.buf = (uint64_t)bswap32(__ldg(aq)) << (32 + 8 * sh);
+    const uint4* aq = reinterpret_cast<const uint4*>(q & ~uintptr_t(15));
+    L.cq = __ldg(aq);
+    L.nq = __ldg(aq + 1);
+    L.qp = aq + 2;
+    L.cw = 4;
+    for (int skip = (int)((q & 15) >> 2); skip > 0; --skip) (void)lane_next_word(L);
+    const int sh = (int)(q & 3);
+    L.buf = (uint64_t)bswap32(lane_next_word(L)) << (32 + 8 * sh);
     L.nb = 32 - 8 * sh;
-    L.wp = aq + 1;
-    L.nxt = __ldg(L.wp);
-    ++L.wp;
     L.slow = L.x < kStateLower;
     return true;
 }
@@ -282,7 +297,10 @@ __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t
 }
 
 template <bool ENTROPY>
-__global__ void __launch_bounds__(K1_THREADS) k1_streams(VolView V, Plan P, unsigned long long* counter) {
+#ifndef K1_MINB
+#define K1_MINB 5
+#endif
+__global__ void __launch_bounds__(K1_THREADS, K1_MINB) k1_streams(VolView V, Plan P, unsigned long long* counter) {
     __shared__ uint32_t tab[2 * 4096];
     if (ENTROPY) {
         for (int i = threadIdx.x; i < 2 * 4096; i += blockDim.x) tab[i] = V.dtab[i];

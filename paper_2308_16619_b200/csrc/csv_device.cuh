@@ -93,6 +93,8 @@ __device__ __forceinline__ uint32_t stream_limit(const VolView& V, uint64_t b, i
 }
 
 __host__ __device__ __forceinline__ uint64_t round16(uint64_t v) { return (v + 15) & ~15ull; }
+__host__ __device__ __forceinline__ uint64_t round32(uint64_t v) { return (v + 31) & ~31ull; }
+constexpr uint64_t kBlobPad = 64;   // readable bytes past every blob (chunk prefetch)
 
 // ---- Morton (x lowest bit, morton.py:3-6) on brick-local indices (<= 21 bits)
 __device__ __forceinline__ uint32_t axis_mask(int a, int bits_per_axis) {

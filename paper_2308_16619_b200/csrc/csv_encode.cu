@@ -715,9 +715,9 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
         ETRY(cudaStreamSynchronize(st));
         uint64_t tp = h[0], tc = h[1] - h[0], td = h[2] - h[1];
         // offsets of parts 1 and 2 are relative to the start of the whole scan: subtract in the kernel via bases
-        ETRY(grow((void**)&enc->d_pal, &enc->cap[0], (pos[0] + tp) * 4 + 16, pos[0] * 4, st));
-        ETRY(grow((void**)&enc->d_coarse, &enc->cap[1], pos[1] + tc + 16, pos[1], st));
-        ETRY(grow((void**)&enc->d_detail, &enc->cap[2], pos[2] + td + 16, pos[2], st));
+        ETRY(grow((void**)&enc->d_pal, &enc->cap[0], (pos[0] + tp) * 4 + kBlobPad, pos[0] * 4, st));
+        ETRY(grow((void**)&enc->d_coarse, &enc->cap[1], pos[1] + tc + kBlobPad, pos[1], st));
+        ETRY(grow((void**)&enc->d_detail, &enc->cap[2], pos[2] + td + kBlobPad, pos[2], st));
         e4_assemble<<<(unsigned)V.nb, 128, 0, st>>>(V, Sc.offs, pos[0], pos[1] - h[0], pos[2] - h[1], enc->d_dir,
                                                       enc->d_pal, enc->d_coarse, enc->d_detail, enc_doff);
         ETRY(cudaGetLastError());
@@ -738,9 +738,9 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
     memcpy(hd + 32, icnt, 32); memcpy(hd + 64, lcnt, 32);
     uint64_t bs[3] = {pos[0] * 4, pos[1], pos[2]}; memcpy(hd + 96, bs, 24);
     // guarantee non-null, padded blobs even when empty
-    if (!enc->d_pal) ETRY(grow((void**)&enc->d_pal, &enc->cap[0], 16, 0, st));
-    if (!enc->d_coarse) ETRY(grow((void**)&enc->d_coarse, &enc->cap[1], 16, 0, st));
-    if (!enc->d_detail) ETRY(grow((void**)&enc->d_detail, &enc->cap[2], 16, 0, st));
+    if (!enc->d_pal) ETRY(grow((void**)&enc->d_pal, &enc->cap[0], kBlobPad, 0, st));
+    if (!enc->d_coarse) ETRY(grow((void**)&enc->d_coarse, &enc->cap[1], kBlobPad, 0, st));
+    if (!enc->d_detail) ETRY(grow((void**)&enc->d_detail, &enc->cap[2], kBlobPad, 0, st));
     *out = enc;
     return cleanup(CSV_OK, "");
 #undef ETRY

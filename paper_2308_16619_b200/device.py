@@ -57,7 +57,7 @@ class GpuVolume:
     ``head120`` is the 120-byte CSV1 head, ``directory`` the structured
     44-byte directory rows of bricks [brick_begin, brick_end), and the blobs
     are numpy arrays (host upload) or torch CUDA tensors (borrowed, with
-    >=16 readable bytes past their end) starting at the given global bases.
+    >=64 readable bytes past their end) starting at the given global bases.
     """
 
     def __init__(self, head120: bytes, directory: np.ndarray, palette, coarse, detail,
