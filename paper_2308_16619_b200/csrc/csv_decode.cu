@@ -359,8 +359,8 @@ __host__ __device__ constexpr Layout make_layout(int L, int idx_bytes) {
     Layout Y{};
     uint32_t nlev = levoffA(L);
     uint32_t maxP = 1u << (3 * (L - 1));              // parents at level t+1 (= children of level t+2)
-    uint32_t ts = L >= 4 ? 4096u : (1u << (3 * L));   // final-level tile (children)
-    uint32_t pbits = maxP > ts ? maxP : ts;
+    uint32_t ts = L >= 4 ? 4096u : (1u << (3 * L));   // final-level tile (children), k2_replay only
+    uint32_t pbits = 8u * maxP;                       // children of the final level
     Y.W = (maxP + 31) / 32;
     Y.lev = 0;
     Y.mask = (nlev + 3) & ~3u;
@@ -370,8 +370,8 @@ __host__ __device__ constexpr Layout make_layout(int L, int idx_bytes) {
     Y.list = Y.ipb + idx_words;
     Y.pend = Y.list + idx_words;
     Y.pax = Y.pend + (pbits + 31) / 32;
-    Y.buf = (Y.pax + (pbits + 15) / 16 + 3) & ~3u;
-    Y.words = Y.buf + ts;
+    Y.buf = (Y.pax + (maxP > ts ? maxP : ts) / 16 + 3) & ~3u;
+    Y.words = idx_bytes == 2 ? Y.buf : Y.buf + ts;    // k2_fast (16-bit) has no tile buffer
     return Y;
 }
 

@@ -14,10 +14,9 @@
 //   T  final level only: the 16^3 tile streamed to HBM (raster or Morton pool)
 
 template <int MODE, int LMAX>
-__global__ void __launch_bounds__(K2_THREADS, 4) k2_fast(VolView V, Plan P) {
+__global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
     static_assert(LMAX <= 5, "shared-memory replay covers N - t <= 5");
     constexpr Layout Y = make_layout(LMAX, 2);
-    constexpr uint32_t TSMAX = LMAX >= 4 ? 4096u : (1u << (3 * LMAX));
     extern __shared__ __align__(16) uint32_t dsm[];
     __shared__ K2Shared S;
     uint16_t* const ipb = reinterpret_cast<uint16_t*>(dsm + Y.ipb);
@@ -120,55 +119,127 @@ __global__ void __launch_bounds__(K2_THREADS, 4) k2_fast(VolView V, Plan P) {
         if (threadIdx.x == 0 && (uint64_t)e0 + 8ull * nact > nvalid)
             atomicMin(&S.errkey, ekey(nvalid, 0, EK_UNDERRUN_NV));
         const uint32_t Cn = 8 * Pn;
-        const uint32_t TS = final_level ? (Cn < TSMAX ? Cn : TSMAX) : Cn;
-        const uint32_t NT = Cn / TS;
-        const uint32_t PT = TS / 8;
-        const uint32_t dst_off = final_level ? Y.buf : Y.lev + levoffA(N - l + 1);
-        for (uint32_t o = 0; o < NT; ++o) {
-            const uint32_t q0 = o * PT, q1 = q0 + PT;
-            const uint32_t j0 = 8 * q0;
-            const uint32_t r0 = dsm[Y.wpre + (q0 >> 5)] + __popc(pmask[q0 >> 5] & ((1u << (q0 & 31)) - 1u));
-            const uint32_t r1 = q1 >= Pn ? nact
-                                         : dsm[Y.wpre + (q1 >> 5)] + __popc(pmask[q1 >> 5] & ((1u << (q1 & 31)) - 1u));
-            for (uint32_t i = threadIdx.x; i < TS / 32; i += K2_THREADS) dsm[Y.pend + i] = 0;
-            for (uint32_t i = threadIdx.x; i < TS / 16; i += K2_THREADS) dsm[Y.pax + i] = 0;
-            __syncthreads();
-            // (C1) active parents of this tile, one lane per parent: the 8 entry
-            // bytes are read at once, all children start as the parent value
-            // (R_p, 2/3 of all entries), and only the other ops are evaluated.
-            for (uint32_t rk = r0 + threadIdx.x; rk < r1; rk += K2_THREADS) {
-                const uint32_t q = list[rk];
-                const uint32_t ent0 = e0 + 8 * rk;
-                const uint64_t w = ent0 + 8 <= ecap ? __ldg(reinterpret_cast<const uint64_t*>(Eb + ent0)) : 0ull;
-                const uint32_t pv = plev[q];
-                uint32_t* const d = dsm + dst_off + 8 * (q - q0);
-                reinterpret_cast<uint4*>(d)[0] = make_uint4(pv, pv, pv, pv);
-                reinterpret_cast<uint4*>(d)[1] = make_uint4(pv, pv, pv, pv);
-                const uint64_t ones = 0x0101010101010101ull;
-                const uint64_t stops = (w >> 3) & ones;
-                if (!final_level) cmask[q] = (uint8_t)~(uint32_t)((stops * 0x0102040810204080ull) >> 56);
-                // flag errors of the whole group first (BAD_OP, LEAF_STOP; codec.py:396-399)
-                const uint32_t nv = nvalid > ent0 ? (nvalid - ent0 < 8 ? nvalid - ent0 : 8) : 0;
-                const uint64_t vmask = nv == 8 ? ~0ull : ((1ull << (8 * nv)) - 1ull);
-                const uint64_t b7 = op_eq(w, 7) & vmask, ls = leaf ? (stops & vmask & ~b7) : 0ull;
-                if (b7 | ls) {
-                    if (b7) atomicMin(&S.errkey, ekey(ent0 + (__ffsll((long long)b7) - 1) / 8, 0, CSV_ST_BAD_OP));
-                    if (ls) atomicMin(&S.errkey, ekey(ent0 + (__ffsll((long long)ls) - 1) / 8, 1, CSV_ST_LEAF_STOP));
+        const int pb = N - l;                        // bits per axis at the parent level
+        const uint32_t pm = (1u << pb) - 1u;
+        const bool al8 = MODE == OUT_RASTER && R.fast && (pitch & 1u) == 0u &&
+                         (reinterpret_cast<uintptr_t>(R.base) & 7u) == 0u;
+        const bool al16 = MODE == OUT_MORTON && (reinterpret_cast<uintptr_t>(out_m) & 15u) == 0u;
+        // storage of child j of this level: shared level array, Morton pool slot or raster voxel
+        auto child_ptr = [&](uint32_t j) -> uint32_t* {
+            if (!final_level) return clev + j;
+            if (MODE == OUT_MORTON) return out_m + j;
+            return raster_of(R, P, j);
+        };
+        // all 8 children of parent q take value v
+        auto fill_group = [&](uint32_t q, uint32_t v) {
+            if (!final_level) {
+                reinterpret_cast<uint4*>(clev + 8 * q)[0] = make_uint4(v, v, v, v);
+                reinterpret_cast<uint4*>(clev + 8 * q)[1] = make_uint4(v, v, v, v);
+            } else if (MODE == OUT_MORTON) {
+                uint32_t* g = out_m + 8ull * q;
+                if (al16) {
+                    reinterpret_cast<uint4*>(g)[0] = make_uint4(v, v, v, v);
+                    reinterpret_cast<uint4*>(g)[1] = make_uint4(v, v, v, v);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) g[c] = v;
                 }
-                const uint64_t pa = op_eq(w, 6);
-                const int32_t ipq = ipbase + (int32_t)ipb[rk];
-                // non-R_p children: bytes whose op is not 0 (op 7 keeps pv; flagged above)
-                uint32_t todo = (uint32_t)(((~op_eq(w, 0) & ones & ~op_eq(w, 7)) * 0x0102040810204080ull) >> 56);
-                while (todo) {
-                    const uint32_t c = __ffs(todo) - 1;
-                    todo &= todo - 1;
-                    const uint32_t e = (uint32_t)(w >> (8 * c)) & 0xFFu;
+            } else if (al8) {
+                uint32_t* g = R.base + ((2 * compact3(q >> 2)) * plane + (2 * compact3(q >> 1)) * pitch + 2 * compact3(q));
+                const uint2 v2 = make_uint2(v, v);
+                *reinterpret_cast<uint2*>(g) = v2;
+                *reinterpret_cast<uint2*>(g + pitch) = v2;
+                *reinterpret_cast<uint2*>(g + plane) = v2;
+                *reinterpret_cast<uint2*>(g + plane + pitch) = v2;
+            } else {
+#pragma unroll
+                for (uint32_t c = 0; c < 8; ++c) {
+                    uint32_t* pp = raster_of(R, P, 8 * q + c);
+                    if (pp) *pp = v;
+                }
+            }
+        };
+        for (uint32_t i = threadIdx.x; i < (Cn + 31) / 32; i += K2_THREADS) dsm[Y.pend + i] = 0;
+        if (!final_level)
+            for (uint32_t i = threadIdx.x; i < (Cn + 15) / 16; i += K2_THREADS) dsm[Y.pax + i] = 0;
+        __syncthreads();
+        // (F0) inactive parents: children repeat the parent value (stop fill, codec.py:460-463);
+        // raster order of parents for raster output so warps write whole row segments
+        for (uint32_t i = threadIdx.x; i < Pn; i += K2_THREADS) {
+            const uint32_t q = (final_level && MODE == OUT_RASTER)
+                ? (spread3_u32(i & pm) | (spread3_u32((i >> pb) & pm) << 1) | (spread3_u32(i >> (2 * pb)) << 2)) : i;
+            if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
+            fill_group(q, plev[q]);
+            if (!final_level) cmask[q] = 0;
+        }
+        // (F1) active parents in 32-parent chunks per warp: each lane sets its
+        // parent's 8 children to the parent value (R_p, 2/3 of all entries), then
+        // the chunk's other children are spread one per lane (warp scan +
+        // shuffle search), evaluated (codec.py:400-457) and stored.
+        {
+            const uint32_t wid = threadIdx.x >> 5;
+            const uint32_t per = (nact + K2_WARPS - 1) / K2_WARPS;
+            const uint32_t wb0 = wid * per, we0 = min(wb0 + per, nact);
+            const uint64_t ones = 0x0101010101010101ull;
+            for (uint32_t cb = wb0; cb < we0; cb += 32) {
+                const uint32_t rk = cb + lane;
+                const bool valid = rk < we0;
+                const uint32_t q = valid ? (uint32_t)list[rk] : 0u;
+                const uint32_t ent0 = e0 + 8 * rk;
+                const uint64_t w = (valid && ent0 + 8 <= ecap) ? __ldg(reinterpret_cast<const uint64_t*>(Eb + ent0)) : 0ull;
+                const uint32_t nv = nvalid > ent0 ? (nvalid - ent0 < 8 ? nvalid - ent0 : 8) : 0;
+                uint32_t todo = 0;
+                int32_t ipq = 0;
+                if (valid) {
+                    fill_group(q, plev[q]);
+                    const uint64_t stops = (w >> 3) & ones;
+                    if (!final_level) cmask[q] = (uint8_t)~(uint32_t)((stops * 0x0102040810204080ull) >> 56);
+                    const uint64_t vmask = nv == 8 ? ~0ull : ((1ull << (8 * nv)) - 1ull);
+                    const uint64_t b7 = op_eq(w, 7) & vmask, ls = leaf ? (stops & vmask & ~b7) : 0ull;
+                    if (b7 | ls) {   // BAD_OP / LEAF_STOP of the whole group (codec.py:396-399)
+                        if (b7) atomicMin(&S.errkey, ekey(ent0 + (__ffsll((long long)b7) - 1) / 8, 0, CSV_ST_BAD_OP));
+                        if (ls) atomicMin(&S.errkey, ekey(ent0 + (__ffsll((long long)ls) - 1) / 8, 1, CSV_ST_LEAF_STOP));
+                    }
+                    todo = (uint32_t)(((~op_eq(w, 0) & ones & ~op_eq(w, 7)) * 0x0102040810204080ull) >> 56);
+                    ipq = ipbase + (int32_t)ipb[rk];
+                }
+                const uint32_t cnt = __popc(todo);
+                uint32_t inc = cnt;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o2);
+                    if (lane >= o2) inc += u;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+                const uint32_t excl = inc - cnt;
+                const uint32_t wlo = (uint32_t)w, whi = (uint32_t)(w >> 32);
+                __syncwarp();
+                for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+                    const uint32_t sidx = k0 + lane;
+                    int src = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const uint32_t ex = __shfl_sync(0xffffffffu, excl, src + step);
+                        if (src + step < 32 && ex <= sidx) src += step;
+                    }
+                    const uint32_t sq = __shfl_sync(0xffffffffu, q, src);
+                    const uint32_t stodo = __shfl_sync(0xffffffffu, todo, src);
+                    const uint32_t sexcl = __shfl_sync(0xffffffffu, excl, src);
+                    const uint32_t slo = __shfl_sync(0xffffffffu, wlo, src);
+                    const uint32_t shi = __shfl_sync(0xffffffffu, whi, src);
+                    const int32_t sip = __shfl_sync(0xffffffffu, ipq, src);
+                    const uint32_t sent0 = __shfl_sync(0xffffffffu, ent0, src);
+                    const uint32_t snv = __shfl_sync(0xffffffffu, nv, src);
+                    if (sidx >= total) continue;
+                    const uint32_t c = __fns(stodo, 0, (int)(sidx - sexcl) + 1);
+                    const uint64_t sw = ((uint64_t)shi << 32) | slo;
+                    const uint32_t e = (uint32_t)(sw >> (8 * c)) & 0xFFu;
                     const uint32_t op = e & 7u;
-                    const uint32_t j = (q << 3) | c;
+                    const uint32_t j = (sq << 3) | c;
                     uint32_t val;
                     int st = 0;
                     bool chain = false;
-                    uint32_t a = op - 1u;
+                    const uint32_t a = op - 1u;
                     if (a < 3u) {
                         const uint32_t M = a == 0 ? Mx : (a == 1 ? My : Mz);
                         const uint32_t part = j & M, rest = j & ~M;
@@ -177,163 +248,80 @@ __global__ void __launch_bounds__(K2_THREADS, 4) k2_fast(VolView V, Plan P) {
                             val = plev[((((part | ~M) + 1u) & M) | rest) >> 3];
                         } else {               // even: the -1 neighbour at this level
                             st = part == 0 ? CSV_ST_BAD_NEIGHBOR : 0;
-                            const uint32_t nb = ((part - 1u) & M) | rest;
-                            const uint32_t qn = nb >> 3;
+                            const uint32_t qn = (((part - 1u) & M) | rest) >> 3;
                             val = plev[qn];    // final when that parent is inactive
                             chain = st == 0 && ((pmask[qn >> 5] >> (qn & 31)) & 1u);
-                            if (chain && nb < j0) {          // earlier tile: already in HBM
-                                chain = false;
-                                const uint32_t* p = MODE == OUT_MORTON ? out_m + nb : raster_of(R, P, nb);
-                                val = p ? *p : 0u;
-                            }
                         }
                     } else {
-                        const int32_t ip = ipq + (int32_t)prefix_bytes(pa, c);
+                        const int32_t ip = sip + (int32_t)prefix_bytes(op_eq(sw, 6), c);
                         int32_t idx = op == 4u ? ip : (op == 5u ? ip - (int32_t)(e >> 4) - 1 : ip + 1);
                         st = idx < 0 ? CSV_ST_DELTA_RANGE : (idx >= (int32_t)plen ? CSV_ST_PALETTE_RANGE : 0);
                         idx = min(max(idx, 0), (int32_t)plen - 1);
                         val = __ldg(pal + idx);
                     }
-                    if (st && c < nv && !(leaf && (e & 8u))) atomicMin(&S.errkey, ekey(ent0 + c, 2, st));
-                    const uint32_t jl = j - j0;
+                    if (st && c < snv && !(leaf && (e & 8u))) atomicMin(&S.errkey, ekey(sent0 + c, 2, st));
                     if (chain) {
-                        atomicOr(&dsm[Y.pend + (jl >> 5)], 1u << (jl & 31));
-                        atomicOr(&dsm[Y.pax + (jl >> 4)], a << (2 * (jl & 15)));
+                        atomicOr(&dsm[Y.pend + (j >> 5)], 1u << (j & 31));
+                        if (!final_level) atomicOr(&dsm[Y.pax + (j >> 4)], a << (2 * (j & 15)));
                     } else {
-                        d[c] = val;
+                        uint32_t* pp = child_ptr(j);
+                        if (pp) *pp = val;
                     }
                 }
             }
-            // (C2) inactive parents of this tile
-            for (uint32_t q = q0 + threadIdx.x; q < q1; q += K2_THREADS) {
-                if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
-                const uint32_t pv = plev[q];
-                uint4* d = reinterpret_cast<uint4*>(dsm + dst_off + 8 * (q - q0));
-                d[0] = make_uint4(pv, pv, pv, pv);
-                d[1] = make_uint4(pv, pv, pv, pv);
-                if (!final_level) cmask[q] = 0;
-            }
-            __syncthreads();
-            // (W) chains: walk -1 neighbours to the first final value (<= 3 hops).
-            // Each warp compacts the pending bits of its words (ballot-free scan
-            // over lanes) so that every lane walks one chain.
-            {
-                const uint32_t NWd = TS / 32;
-                const uint32_t wpw = (NWd + K2_WARPS - 1) / K2_WARPS;
-                const uint32_t wbeg = (threadIdx.x >> 5) * wpw, wend = min(wbeg + wpw, NWd);
-                for (uint32_t wb = wbeg; wb < wend; wb += 32) {
-                    const uint32_t wi = wb + lane;
-                    const uint32_t word = wi < wend ? dsm[Y.pend + wi] : 0u;
-                    const uint32_t cnt = __popc(word);
-                    uint32_t inc = cnt;
-#pragma unroll
-                    for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o2);
-                        if (lane >= o2) inc += u;
-                    }
-                    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-                    const uint32_t excl = inc - cnt;
-                    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-                        const uint32_t sidx = k0 + lane;
-                        int src = 0;
-#pragma unroll
-                        for (int step = 16; step > 0; step >>= 1) {
-                            const uint32_t ex = __shfl_sync(0xffffffffu, excl, src + step);
-                            if (src + step < 32 && ex <= sidx) src += step;
-                        }
-                        const uint32_t wsrc = __shfl_sync(0xffffffffu, word, src);
-                        const uint32_t esrc = __shfl_sync(0xffffffffu, excl, src);
-                        if (sidx >= total) continue;
-                        const uint32_t jl = 32 * (wb + src) + __fns(wsrc, 0, (int)(sidx - esrc) + 1);
-                        uint32_t cl = jl;
-#pragma unroll 1
-                        for (int hop = 0; hop < 4; ++hop) {
-                            const uint32_t aa = (dsm[Y.pax + (cl >> 4)] >> (2 * (cl & 15))) & 3u;
-                            const uint32_t MM = aa == 0 ? Mx : (aa == 1 ? My : Mz);
-                            const uint32_t jg = cl + j0;
-                            cl = ((((jg & MM) - 1u) & MM) | (jg & ~MM)) - j0;
-                            if (!((dsm[Y.pend + (cl >> 5)] >> (cl & 31)) & 1u)) break;
-                        }
-                        dsm[dst_off + jl] = dsm[dst_off + cl];
-                    }
-                }
-            }
-            __syncthreads();
-            if (!final_level) continue;
-            // (T) stream the tile to HBM
-            if (MODE == OUT_MORTON) {
-                uint32_t* d = out_m + (size_t)TS * o;
-                const bool al = (reinterpret_cast<uintptr_t>(d) & 15) == 0;
-                for (uint32_t i = threadIdx.x; i < TS / 4; i += K2_THREADS) {
-                    const uint4 v = reinterpret_cast<const uint4*>(dsm + Y.buf)[i];
-                    if (al) reinterpret_cast<uint4*>(d)[i] = v;
-                    else { d[4 * i] = v.x; d[4 * i + 1] = v.y; d[4 * i + 2] = v.z; d[4 * i + 3] = v.w; }
-                }
-            } else if (TS == 4096 && R.fast) {
-                // 16^3 tile: lane = (x-group 4, y0y1 4, z0 2); each lane reads its 4
-                // x-consecutive voxels rotated by its x-group so every LDS hits 32
-                // distinct banks, then writes them as one 16-byte row segment
-                const uint32_t xg = lane & 3, y01 = (lane >> 2) & 3, z0 = (lane >> 4) & 1;
-                const uint32_t ox = (compact3(o) << 4) + 4 * xg;
-                const uint32_t oy = compact3(o >> 1) << 4, oz = compact3(o >> 2) << 4;
-                const uint32_t mx = spread3_u32(4 * xg);
-                const uint32_t s0 = spread3_u32(xg & 3), s1 = spread3_u32((xg + 1) & 3),
-                               s2 = spread3_u32((xg + 2) & 3), s3 = spread3_u32((xg + 3) & 3);
-                const bool al = ((pitch & 3u) == 0u) && ((reinterpret_cast<uintptr_t>(R.base) & 15u) == 0u);
-                auto tile_rows = [&](auto vec) {
-#pragma unroll
-                    for (int it = 0; it < 4; ++it) {
-                        const uint32_t combo = (threadIdx.x >> 5) * 4 + it;      // 0..31
-                        const uint32_t y = y01 | ((combo & 3) << 2), z = z0 | ((combo >> 2) << 1);
-                        const uint32_t mb = (spread3_u32(y) << 1) | (spread3_u32(z) << 2) | mx;
-                        const uint32_t u0 = dsm[Y.buf + (mb | s0)], u1 = dsm[Y.buf + (mb | s1)],
-                                       u2 = dsm[Y.buf + (mb | s2)], u3 = dsm[Y.buf + (mb | s3)];
-                        // un-rotate: v[x] = u[(x - xg) & 3]
-                        uint32_t v0 = u0, v1 = u1, v2 = u2, v3 = u3;
-                        if (xg & 1) { uint32_t tt = v3; v3 = v2; v2 = v1; v1 = v0; v0 = tt; }
-                        if (xg & 2) { uint32_t t0 = v0, t1 = v1; v0 = v2; v1 = v3; v2 = t0; v3 = t1; }
-                        uint32_t* p = R.base + ((oz + z) * plane + (oy + y) * pitch + ox);
-                        if (decltype(vec)::value) {
-                            *reinterpret_cast<uint4*>(p) = make_uint4(v0, v1, v2, v3);
-                        } else {
-                            asm volatile("st.global.v2.u32 [%0], {%1, %2};" :: "l"(p), "r"(v0), "r"(v1) : "memory");
-                            asm volatile("st.global.v2.u32 [%0], {%1, %2};" :: "l"(p + 2), "r"(v2), "r"(v3) : "memory");
-                        }
-                    }
-                };
-                if (al) tile_rows(std::true_type{});
-                else if ((pitch & 1u) == 0u && (reinterpret_cast<uintptr_t>(R.base) & 7u) == 0u) tile_rows(std::false_type{});
-                else {
-                    for (int it = 0; it < 4; ++it) {
-                        const uint32_t combo = (threadIdx.x >> 5) * 4 + it;
-                        const uint32_t y = y01 | ((combo & 3) << 2), z = z0 | ((combo >> 2) << 1);
-                        const uint32_t mb = (spread3_u32(y) << 1) | (spread3_u32(z) << 2) | mx;
-                        uint32_t* p = R.base + ((oz + z) * plane + (oy + y) * pitch + ox);
-#pragma unroll
-                        for (uint32_t k = 0; k < 4; ++k) {
-                            const uint32_t v = dsm[Y.buf + (mb | spread3_u32(k))];
-                            asm volatile("st.global.u32 [%0], %1;" :: "l"(p + k), "r"(v) : "memory");
-                        }
-                    }
-                }
-            } else {
-                const int tb = (31 - __clz(TS)) / 3;          // log2 of the tile side
-                const uint32_t ts = 1u << tb;
-                const uint32_t tx = compact3(o) << tb, ty = compact3(o >> 1) << tb, tz = compact3(o >> 2) << tb;
-                for (uint32_t i = threadIdx.x; i < TS; i += K2_THREADS) {
-                    const uint32_t x = i & (ts - 1), y = (i >> tb) & (ts - 1), z = i >> (2 * tb);
-                    const uint32_t v = dsm[Y.buf + (spread3_u32(x) | (spread3_u32(y) << 1) | (spread3_u32(z) << 2))];
-                    if (R.fast) {
-                        R.base[(tz + z) * plane + (ty + y) * pitch + tx + x] = v;
-                    } else {
-                        const int64_t gx = R.ox + tx + x, gy = R.oy + ty + y, gz = R.oz + tz + z;
-                        if (gz >= P.z_begin && gz < P.z_end && gy < P.cy && gx < P.cx)
-                            P.out[((gz - P.z_begin) * P.cy + gy) * P.cx + gx] = v;
-                    }
-                }
-            }
-            __syncthreads();
         }
+        __syncthreads();
+        // (W) chains (codec.py:422-423, nm < j): walk -1 neighbours (<= 3 hops, each
+        // makes one more coordinate odd) to the first child whose value is final
+        if (S.errkey == ~0ull) {
+            const uint32_t NWd = (Cn + 31) / 32;
+            const uint32_t wpw = (NWd + K2_WARPS - 1) / K2_WARPS;
+            const uint32_t wbeg = (threadIdx.x >> 5) * wpw, wend = min(wbeg + wpw, NWd);
+            for (uint32_t wb = wbeg; wb < wend; wb += 32) {
+                const uint32_t wi = wb + lane;
+                const uint32_t word = wi < wend ? dsm[Y.pend + wi] : 0u;
+                const uint32_t cnt = __popc(word);
+                uint32_t inc = cnt;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o2);
+                    if (lane >= o2) inc += u;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+                const uint32_t excl = inc - cnt;
+                for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+                    const uint32_t sidx = k0 + lane;
+                    int src = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const uint32_t ex = __shfl_sync(0xffffffffu, excl, src + step);
+                        if (src + step < 32 && ex <= sidx) src += step;
+                    }
+                    const uint32_t wsrc = __shfl_sync(0xffffffffu, word, src);
+                    const uint32_t esrc = __shfl_sync(0xffffffffu, excl, src);
+                    if (sidx >= total) continue;
+                    const uint32_t j = 32 * (wb + src) + __fns(wsrc, 0, (int)(sidx - esrc) + 1);
+                    uint32_t cl = j;
+#pragma unroll 1
+                    for (int hop = 0; hop < 4; ++hop) {
+                        uint32_t aa;
+                        if (!final_level) {
+                            aa = (dsm[Y.pax + (cl >> 4)] >> (2 * (cl & 15))) & 3u;
+                        } else {
+                            const uint32_t qc = cl >> 3;
+                            const uint32_t rkc = dsm[Y.wpre + (qc >> 5)] + __popc(pmask[qc >> 5] & ((1u << (qc & 31)) - 1u));
+                            aa = (__ldg(Eb + e0 + 8 * rkc + (cl & 7)) & 7u) - 1u;
+                        }
+                        const uint32_t MM = aa == 0 ? Mx : (aa == 1 ? My : Mz);
+                        cl = (((cl & MM) - 1u) & MM) | (cl & ~MM);
+                        if (!((dsm[Y.pend + (cl >> 5)] >> (cl & 31)) & 1u)) break;
+                    }
+                    uint32_t* d = child_ptr(j);
+                    if (d) *d = *child_ptr(cl);
+                }
+            }
+        }
+        __syncthreads();
         const unsigned long long ek = S.errkey;
         if (ek != ~0ull) {
             const csv_stream_result& sr = leaf ? srd : src;
