@@ -387,6 +387,7 @@ enum { EK_UNDERRUN_NV = 15 };   // status placeholder: entry == K1's n_entries
 struct K2Shared {
     unsigned long long errkey;
     uint32_t scan[K2_WARPS + 1];
+    uint32_t scan2[K2_WARPS + 1];
     uint64_t red64[2][K2_WARPS];
 };
 

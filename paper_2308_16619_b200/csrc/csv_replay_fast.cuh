@@ -13,6 +13,20 @@
 //   W  same-level chains (even-coordinate reuse, :422-423) walked in smem
 //   T  final level only: the 16^3 tile streamed to HBM (raster or Morton pool)
 
+// position of the r-th (0-based) set bit of m (r < popc(m)); branch-free bisection
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t m, uint32_t r) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int width = 16; width > 0; width >>= 1) {
+        const uint32_t lo = __popc(m & ((1u << width) - 1u));
+        const bool up = r >= lo;
+        r -= up ? lo : 0u;
+        m = up ? (m >> width) : m;
+        pos += up ? (uint32_t)width : 0u;
+    }
+    return pos;
+}
+
 template <int MODE, int LMAX>
 __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
     static_assert(LMAX <= 5, "shared-memory replay covers N - t <= 5");
@@ -89,35 +103,87 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
         const uint32_t nvalid = leaf ? srd.n_entries : src.n_entries;
         const int cbits = N - l + 1;
         const uint32_t Mx = axis_mask(0, cbits), My = axis_mask(1, cbits), Mz = axis_mask(2, cbits);
-        // (A) rank prefix of active parents
-        for (uint32_t i = threadIdx.x; i < W; i += K2_THREADS) {
-            uint32_t mw = pmask[i];
-            if (Pn < 32) mw &= (1u << Pn) - 1u;
-            pmask[i] = mw;
-            dsm[Y.wpre + i] = __popc(mw);
+        // (A) rank prefix of the active-parent bitmask: each warp scans its own
+        // contiguous word range, one barrier, then adds the preceding warps' totals
+        const uint32_t wid = threadIdx.x >> 5;
+        if (Pn < 32 && threadIdx.x == 0) pmask[0] &= (1u << Pn) - 1u;
+        if (Pn < 32) __syncwarp();
+        const uint32_t cw = (W + K2_WARPS - 1) / K2_WARPS;
+        const uint32_t wb = min(wid * cw, W), we = min(wb + cw, W);
+        {
+            uint32_t run = 0;
+            for (uint32_t c0 = wb; c0 < we; c0 += 32) {
+                const uint32_t i = c0 + lane;
+                const uint32_t v = i < we ? __popc(pmask[i]) : 0u;
+                uint32_t inc = v;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o2);
+                    if (lane >= o2) inc += u;
+                }
+                if (i < we) dsm[Y.wpre + i] = run + inc - v;
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if (lane == 0) S.scan[wid] = run;
         }
         __syncthreads();
-        const uint32_t nact = block_scan_inplace(dsm + Y.wpre, W, S);
-        // (B) active list + palette-advance counts per active parent
-        for (uint32_t i = threadIdx.x; i < W; i += K2_THREADS) {
-            uint32_t mw = pmask[i], rk = dsm[Y.wpre + i];
+        uint32_t nact = 0, woff = 0;
+#pragma unroll
+        for (int k = 0; k < K2_WARPS; ++k) {
+            const uint32_t v = S.scan[k];
+            woff += (uint32_t)k < wid ? v : 0u;
+            nact += v;
+        }
+        // (B) active list (rank -> parent) and palette-advance counts per active
+        // parent, scanned the same way; F1 below reads only its own warp's ranks
+        for (uint32_t i = wb + lane; i < we; i += 32) {
+            uint32_t mw = pmask[i], rk = dsm[Y.wpre + i] + woff;
+            dsm[Y.wpre + i] = rk;
             while (mw) {
                 list[rk++] = (uint16_t)(32 * i + (__ffs(mw) - 1));
                 mw &= mw - 1;
             }
         }
-        uint32_t pdl = 0;
-        for (uint32_t i = threadIdx.x; i < nact; i += K2_THREADS) {
-            const uint32_t off = e0 + 8 * i;
-            const uint64_t w = off + 8 <= ecap ? __ldg(reinterpret_cast<const uint64_t*>(Eb + off)) : 0ull;
-            ipb[i] = (uint16_t)__popcll(op_eq(w, 6));
-            pdl += __popcll(op_eq(w, 5));
+        const uint32_t cr = (nact + K2_WARPS - 1) / K2_WARPS;
+        const uint32_t rb = min(wid * cr, nact), re = min(rb + cr, nact);
+        {
+            uint32_t run = 0, pdl = 0;
+            for (uint32_t c0 = rb; c0 < re; c0 += 32) {
+                const uint32_t i = c0 + lane;
+                const uint32_t off = e0 + 8 * i;
+                const uint64_t w = (i < re && off + 8 <= ecap) ? __ldg(reinterpret_cast<const uint64_t*>(Eb + off)) : 0ull;
+                const uint32_t v = __popcll(op_eq(w, 6));
+                pdl += __popcll(op_eq(w, 5));
+                uint32_t inc = v;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o2);
+                    if (lane >= o2) inc += u;
+                }
+                if (i < re) ipb[i] = (uint16_t)(run + inc - v);
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if (lane == 0) S.scan2[wid] = run;
+            if (leaf) pd_d += pdl; else pd_c += pdl;
         }
-        if (leaf) pd_d += pdl; else pd_c += pdl;
-        __syncthreads();
-        const uint32_t tot_pa = block_scan_inplace(ipb, nact, S);
+        {
+            const uint32_t Cn0 = 8 * Pn;
+            for (uint32_t i = threadIdx.x; i < (Cn0 + 31) / 32; i += K2_THREADS) dsm[Y.pend + i] = 0;
+            if (!final_level)
+                for (uint32_t i = threadIdx.x; i < (Cn0 + 15) / 16; i += K2_THREADS) dsm[Y.pax + i] = 0;
+        }
         if (threadIdx.x == 0 && (uint64_t)e0 + 8ull * nact > nvalid)
             atomicMin(&S.errkey, ekey(nvalid, 0, EK_UNDERRUN_NV));
+        __syncthreads();
+        uint32_t tot_pa = 0, ioff = 0;
+#pragma unroll
+        for (int k = 0; k < K2_WARPS; ++k) {
+            const uint32_t v = S.scan2[k];
+            ioff += (uint32_t)k < wid ? v : 0u;
+            tot_pa += v;
+        }
+        for (uint32_t i = rb + lane; i < re; i += 32) ipb[i] = (uint16_t)(ipb[i] + ioff);
+        __syncwarp();
         const uint32_t Cn = 8 * Pn;
         const int pb = N - l;                        // bits per axis at the parent level
         const uint32_t pm = (1u << pb) - 1u;
@@ -159,10 +225,6 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
                 }
             }
         };
-        for (uint32_t i = threadIdx.x; i < (Cn + 31) / 32; i += K2_THREADS) dsm[Y.pend + i] = 0;
-        if (!final_level)
-            for (uint32_t i = threadIdx.x; i < (Cn + 15) / 16; i += K2_THREADS) dsm[Y.pax + i] = 0;
-        __syncthreads();
         // (F0) inactive parents: children repeat the parent value (stop fill, codec.py:460-463);
         // raster order of parents for raster output so warps write whole row segments
         for (uint32_t i = threadIdx.x; i < Pn; i += K2_THREADS) {
@@ -177,9 +239,7 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
         // the chunk's other children are spread one per lane (warp scan +
         // shuffle search), evaluated (codec.py:400-457) and stored.
         {
-            const uint32_t wid = threadIdx.x >> 5;
-            const uint32_t per = (nact + K2_WARPS - 1) / K2_WARPS;
-            const uint32_t wb0 = wid * per, we0 = min(wb0 + per, nact);
+            const uint32_t wb0 = rb, we0 = re;          // same rank partition as (B)
             const uint64_t ones = 0x0101010101010101ull;
             for (uint32_t cb = wb0; cb < we0; cb += 32) {
                 const uint32_t rk = cb + lane;
@@ -231,7 +291,7 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
                     const uint32_t sent0 = __shfl_sync(0xffffffffu, ent0, src);
                     const uint32_t snv = __shfl_sync(0xffffffffu, nv, src);
                     if (sidx >= total) continue;
-                    const uint32_t c = __fns(stodo, 0, (int)(sidx - sexcl) + 1);
+                    const uint32_t c = nth_set_bit(stodo, sidx - sexcl);
                     const uint64_t sw = ((uint64_t)shi << 32) | slo;
                     const uint32_t e = (uint32_t)(sw >> (8 * c)) & 0xFFu;
                     const uint32_t op = e & 7u;
@@ -300,7 +360,7 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
                     const uint32_t wsrc = __shfl_sync(0xffffffffu, word, src);
                     const uint32_t esrc = __shfl_sync(0xffffffffu, excl, src);
                     if (sidx >= total) continue;
-                    const uint32_t j = 32 * (wb + src) + __fns(wsrc, 0, (int)(sidx - esrc) + 1);
+                    const uint32_t j = 32 * (wb + src) + nth_set_bit(wsrc, sidx - esrc);
                     uint32_t cl = j;
 #pragma unroll 1
                     for (int hop = 0; hop < 4; ++hop) {
