@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
         R.oy = (int64_t)((gb / V.gx) % V.gy) * side;
         R.oz = (int64_t)(gb / (V.gx * V.gy)) * side;
         R.base = P.out + ((R.oz - P.z_begin) * P.cy + R.oy) * P.cx + R.ox;
+        asm volatile("" : "+l"(R.base));   // computed once: keep it in registers, not rematerialised
         R.fast = R.ox + side <= P.cx && R.oy + side <= P.cy && R.oz >= P.z_begin && R.oz + side <= P.z_end &&
                  (uint64_t)P.cx * P.cy * side < (1ull << 32);
         pitch = (uint32_t)P.cx;
@@ -227,12 +228,27 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
         };
         // (F0) inactive parents: children repeat the parent value (stop fill, codec.py:460-463);
         // raster order of parents for raster output so warps write whole row segments
-        for (uint32_t i = threadIdx.x; i < Pn; i += K2_THREADS) {
-            const uint32_t q = (final_level && MODE == OUT_RASTER)
-                ? (spread3_u32(i & pm) | (spread3_u32((i >> pb) & pm) << 1) | (spread3_u32(i >> (2 * pb)) << 2)) : i;
-            if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
-            fill_group(q, plev[q]);
-            if (!final_level) cmask[q] = 0;
+        if (final_level && MODE == OUT_RASTER && al8) {
+            for (uint32_t i = threadIdx.x; i < Pn; i += K2_THREADS) {
+                const uint32_t qx = i & pm, qy = (i >> pb) & pm, qz = i >> (2 * pb);
+                const uint32_t q = spread3_u32(qx) | (spread3_u32(qy) << 1) | (spread3_u32(qz) << 2);
+                if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
+                const uint32_t v = plev[q];
+                uint32_t* g = R.base + ((2 * qz) * plane + (2 * qy) * pitch + 2 * qx);
+                const uint2 v2 = make_uint2(v, v);
+                *reinterpret_cast<uint2*>(g) = v2;
+                *reinterpret_cast<uint2*>(g + pitch) = v2;
+                *reinterpret_cast<uint2*>(g + plane) = v2;
+                *reinterpret_cast<uint2*>(g + plane + pitch) = v2;
+            }
+        } else {
+            for (uint32_t i = threadIdx.x; i < Pn; i += K2_THREADS) {
+                const uint32_t q = (final_level && MODE == OUT_RASTER)
+                    ? (spread3_u32(i & pm) | (spread3_u32((i >> pb) & pm) << 1) | (spread3_u32(i >> (2 * pb)) << 2)) : i;
+                if ((pmask[q >> 5] >> (q & 31)) & 1u) continue;
+                fill_group(q, plev[q]);
+                if (!final_level) cmask[q] = 0;
+            }
         }
         // (F1) active parents in 32-parent chunks per warp: each lane sets its
         // parent's 8 children to the parent value (R_p, 2/3 of all entries), then
