@@ -213,6 +213,43 @@ def desired_lods(grid, b, cam, fov, height, max_lod):
     return lod, d
 
 
+# ---------------------------------------------------------------------------- config 5
+def timeseries_leg(p, torch, dev, stream, steps: int = 2, dims=(1024, 1024, 1024), cells: int = 22):
+    """1024^3 Voronoi timesteps (seed 3, seeds drifting
+    by <= k voxels at step k); per timestep GPU encode then GPU decode, both
+    timed with CUDA events; lossless round trip checked (untimed)."""
+    enc_ms, dec_ms = [], []
+    X, Y, Z = dims
+    for k in range(steps):
+        vol = p.synth_voronoi(dims, cells, seed=3, membrane=False, drift=float(min(k, 16)), drift_seed=3 + k,
+                              device=dev)
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        enc = p.compress_volume_device(vol, p.CompressionConfig(brick_log2=BRICK_LOG2))
+        e1.record(stream)
+        gv = enc.to_volume()
+        out = torch.empty_like(vol)
+        torch.cuda.synchronize()
+        e1b = torch.cuda.Event(enable_timing=True)
+        e1b.record(stream)
+        gv.decode(0, out=out)
+        e2.record(stream)
+        torch.cuda.synchronize()
+        assert torch.equal(out, vol), "time-series round trip mismatch"
+        enc_ms.append(e0.elapsed_time(e1))
+        dec_ms.append(e1b.elapsed_time(e2))
+        gv.close()
+        enc.close()
+        del vol, out
+        torch.cuda.empty_cache()
+    vox = X * Y * Z * steps
+    te, td = sum(enc_ms) / 1e3, sum(dec_ms) / 1e3
+    return {"timesteps": steps, "dims": list(dims), "encode_gvox_s": vox / te / 1e9, "decode_gvox_s": vox / td / 1e9,
+            "roundtrip_gvox_s": vox / (te + td) / 1e9, "encode_ms": enc_ms, "decode_ms": dec_ms,
+            "workload": "config 5 share of one GPU: 2 of 16 timesteps of 1024^3 Voronoi (22^3 cells, seed 3, drift <= k)"}
+
+
 # ---------------------------------------------------------------------------- our arm
 def run_ours(args, world, rank, local):
     import torch
@@ -358,6 +395,9 @@ def run_ours(args, world, rank, local):
                                             "csv_decode_bricks batch into an 8 GiB device pool"}
         full.close()
         del cache
+    # ---- config 5: time series encode + decode (2 timesteps = one GPU's share of 16 over 8 GPUs)
+    if not args.no_cache and not args.profile and world == 1 and args.workload == "config3" and not args.zlayers:
+        line["timeseries"] = timeseries_leg(p, torch, dev, stream)
     # ---- e2e: public API, host buffers in, host volume out (pinned)
     if not args.no_e2e and not args.profile:
         pin = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32, pin_memory=True)

@@ -139,6 +139,13 @@ int csv_decode_streams(csv_volume* vol, uint64_t n, const uint32_t* d_brick, int
 /* Upper bound of the entry bytes csv_decode_streams needs for n requests at LOD t. */
 int csv_streams_capacity(csv_volume* vol, uint64_t n, int t, uint64_t* cap);
 
+/* Operation histogram of every brick's full streams (stats(), container.py:485-529):
+ * d_counts8[op] = number of entries with opcode op (payload nibbles excluded);
+ * d_sres (2 x bricks, coarse then detail per brick) reports truncated (FAILED
+ * before COMPLETE) and desynchronized streams as rans_decode would
+ * (rans.py:183-198).  No entry buffer is written. */
+int csv_volume_op_counts(csv_volume* vol, uint64_t* d_counts8, csv_stream_result* d_sres, uintptr_t stream);
+
 /* Volume geometry probe: dims(x,y,z), grid(x,y,z), brick_log2, entropy. */
 int csv_volume_info(csv_volume* vol, int64_t* dims3, int64_t* grid3, int* brick_log2, int* entropy);
 

@@ -9,7 +9,7 @@ kernels (csrc/) reached through the C-ABI in include/csvgpu.h.
 from .cache import BrickCache, CacheStats
 from .codec import BrickEncoding, decode_brick, decode_brick_entropy, decode_root, iter_operations
 from .container import (CompressionConfig, CsvContainer, VolumeMeta, decompress_volume,
-                        decompress_volume_device)
+                        decompress_volume_device, stats)
 from .device import GpuVolume
 from .encode import GpuEncoded, compress_volume, compress_volume_device, synth_voronoi
 from .errors import (CacheCapacityError, ConfigError, CorruptStreamError, CsvolError, EncodabilityError,
@@ -24,5 +24,5 @@ __all__ = [
     "ConfigError", "CorruptStreamError", "CsvContainer", "CsvolError", "EncodabilityError", "FrequencyTable",
     "GpuEncoded", "GpuVolume", "compress_volume", "compress_volume_device", "synth_voronoi", "IngestionError", "NodeCoord", "TablePair", "VolumeMeta", "build_frequency_tables",
     "decode_brick", "decode_brick_entropy", "decode_root", "decompress_volume", "decompress_volume_device",
-    "iter_operations", "morton_decode", "morton_encode", "outside_neighbor", "quantize_counts",
+    "iter_operations", "stats", "morton_decode", "morton_encode", "outside_neighbor", "quantize_counts",
 ]

@@ -322,3 +322,85 @@ def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None =
     import torch
     torch.from_numpy(out.view(np.int32)).copy_(dev)
     return out
+
+
+# ------------------------------------------------------------------------------ statistics
+_OP_NAMES = ("parent", "neighbor_x", "neighbor_y", "neighbor_z", "palette_last", "palette_back", "palette_advance")
+
+
+def stats(container: CsvContainer) -> dict:
+    """Volume statistics (container.py:498-555): the operation histogram comes
+    from the K1 entropy lanes in count mode (csv_volume_op_counts), the per-brick
+    rates and palette duplicates from the directory on the host."""
+    from .device import GpuVolume   # noqa: F401
+    from . import _lib
+    meta = container.meta
+    d = container.directory
+    n = meta.brick_count
+    cn = d["coarse_nibbles"].astype(np.int64)
+    dn = d["detail_nibbles"].astype(np.int64)
+    vol = container.to_device()
+    try:
+        counts, sres = vol.op_counts()
+    finally:
+        vol.close()
+    if meta.entropy:
+        # first failing stream in the reference's order: brick by brick, coarse then detail (rans.py:183-198)
+        fl = sres["flags"].reshape(n, 2)
+        fn = sres["fail_nibble"].reshape(n, 2)
+        nn = np.stack([cn, dn], axis=1)
+        trunc = (nn > 0) & ((fl & 1) != 0) & ((fl & 8) == 0)
+        desync = (nn > 0) & ((fl & 4) != 0)
+        bad = trunc | desync
+        if bad.any():
+            k = int(np.flatnonzero(bad.reshape(-1))[0])
+            i, s = divmod(k, 2)
+            if trunc[i, s]:
+                raise CorruptStreamError(f"entropy stream truncated at symbol {int(fn[i, s])}")
+            raise CorruptStreamError(f"entropy stream desynchronized after {int(nn[i, s])} symbols")
+    op_counts = counts.astype(np.int64)
+    brick_bytes_orig = meta.brick_side ** 3 * (meta.width // 8)
+    payload = d["palette_len"].astype(np.int64) * 4 + d["coarse_bytes"].astype(np.int64) + d["detail_bytes"].astype(np.int64)
+    brick_cr = payload / brick_bytes_orig
+    # palette slices exactly as brick_palette() takes them (numpy slice clamping)
+    off = d["palette_off"].astype(np.int64)
+    lens = np.clip(np.minimum(off + d["palette_len"].astype(np.int64), container.palette_blob.size) - off, 0, None)
+    lens = np.where(off < container.palette_blob.size, lens, 0)
+    tot = int(lens.sum())
+    if tot:
+        starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        idx = np.arange(tot) - np.repeat(starts - off, lens)
+        vals = container.palette_blob[idx]
+        bid = np.repeat(np.arange(n), lens)
+        order = np.lexsort((vals, bid))
+        vs, bs = vals[order], bid[order]
+        new = np.ones(tot, dtype=bool)
+        new[1:] = (vs[1:] != vs[:-1]) | (bs[1:] != bs[:-1])
+        uniq = np.bincount(bs[new], minlength=n)
+    else:
+        uniq = np.zeros(n, dtype=np.int64)
+    duplicates = lens - uniq
+    homogeneous = int(((lens == 1) & (cn == 0) & (dn == 0)).sum())
+    total_ops = max(int(op_counts.sum()), 1)
+    frequencies = {_OP_NAMES[op]: int(op_counts[op]) / total_ops for op in range(7)}
+    reuse = sum(frequencies[_OP_NAMES[op]] for op in range(4))
+    edges = np.array([0.0] + [2.0 ** e for e in range(-14, 1)])
+    hist, _ = np.histogram(brick_cr, bins=edges)
+    dup_vals, dup_counts = np.unique(duplicates, return_counts=True)
+    return {
+        "dims": meta.dims,
+        "brick_side": meta.brick_side,
+        "brick_count": meta.brick_count,
+        "entropy": meta.entropy,
+        "original_bytes": meta.original_bytes,
+        "payload_bytes": container.payload_bytes,
+        "compression_rate": container.compression_rate,
+        "op_frequencies": frequencies,
+        "reuse_fraction": reuse,
+        "total_ops": total_ops,
+        "brick_cr_histogram": {"edges": edges.tolist(), "counts": hist.tolist()},
+        "brick_cr_max": float(brick_cr.max()) if brick_cr.size else 0.0,
+        "homogeneous_bricks": homogeneous,
+        "palette_duplicates": dict(zip(dup_vals.tolist(), dup_counts.tolist())),
+        "mean_palette_duplicates": float(duplicates.mean()) if duplicates.size else 0.0,
+    }

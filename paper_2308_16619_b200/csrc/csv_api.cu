@@ -20,6 +20,7 @@ cudaError_t run_root_raster(const VolView& V, Plan P, cudaStream_t st);
 cudaError_t run_streams_only(const VolView& V, Plan P, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                              unsigned long long* counter, int nsm, cudaStream_t st);
 size_t k2_smem_bytes(int L);
+cudaError_t run_op_counts(const VolView& V, Plan P, unsigned long long* counter, int nsm, cudaStream_t st);
 uint64_t k2_gws_words(int L);
 }  // namespace csv
 
@@ -428,6 +429,22 @@ int csv_volume_get_timing(csv_volume* vol, float* ms3) {
     CUDA_TRY(cudaEventElapsedTime(&ms3[0], vol->ev[0], vol->ev[1]));
     CUDA_TRY(cudaEventElapsedTime(&ms3[1], vol->ev[1], vol->ev[2]));
     CUDA_TRY(cudaEventElapsedTime(&ms3[2], vol->ev[2], vol->ev[3]));
+    return CSV_OK;
+}
+
+int csv_volume_op_counts(csv_volume* vol, uint64_t* d_counts8, csv_stream_result* d_sres, uintptr_t stream) {
+    if (!vol || !d_counts8 || !d_sres) return fail(CSV_E_ARG, "null argument");
+    CUDA_TRY(cudaSetDevice(vol->device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int rc = ensure_plan(vol, vol->V.nb, 0, 0, st);
+    if (rc) return rc;
+    Plan P{};
+    P.n = vol->V.nb;
+    P.t_uniform = 0;
+    P.sres = d_sres;
+    P.op_counts = reinterpret_cast<unsigned long long*>(d_counts8);
+    CUDA_TRY(cudaMemsetAsync(d_counts8, 0, 8 * sizeof(uint64_t), st));
+    CUDA_TRY(run_op_counts(vol->V, P, vol->d_counter, vol->nsm, st));
     return CSV_OK;
 }
 

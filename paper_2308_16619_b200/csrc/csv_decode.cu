@@ -126,6 +126,7 @@ struct Lane {
     uint64_t buf;           // upcoming stream bits, MSB first
     uint64_t acc;           // entry bytes of the group being built (<= 8)
     uint64_t* outp;         // entry region (32-byte aligned)
+    uint64_t c03, c47;      // count mode: per-op counters, 4 x 16 bits each
     const uint8_t* rawp;    // raw mode: packed nibble bytes
     uint32_t x;             // rANS state (fits 32 bits: f*(x>>12) < 2^32)
     uint32_t pos, len;      // bytes consumed (incl. 4 state bytes) / stream bytes
@@ -137,6 +138,7 @@ struct Lane {
     int cw;                 // words left in cq
     int k;                  // entries in acc
     int tsel;               // decode table (0 interior, 1 leaf)
+    uint32_t since;         // count mode: ops since the last flush
     bool pend;              // next nibble is a P_delta payload
     bool slow;              // first step from a state < 2^23 (corrupt streams only)
 };
@@ -161,9 +163,28 @@ __device__ __forceinline__ void lane_refill(Lane& L) {
     L.nb += 32;
 }
 
+// count-mode flush of the packed per-op counters (stats(), container.py:485-495)
+__device__ __forceinline__ void lane_flush_counts(Lane& L, unsigned long long* counts) {
+#pragma unroll
+    for (int op = 0; op < 8; ++op) {
+        const uint64_t v = ((op < 4 ? L.c03 : L.c47) >> (16 * (op & 3))) & 0xFFFFull;
+        if (v) atomicAdd(counts + op, (unsigned long long)v);
+    }
+    L.c03 = 0; L.c47 = 0; L.since = 0;
+}
+
+template <bool COUNT>
 __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
     bool pay = L.pend;
     L.pend = !pay && ((s & 7u) == 5u);
+    if (COUNT) {   // every op nibble counts, its payload does not (container.py:485-495)
+        if (!pay) {
+            const uint64_t inc = 1ull << (16 * (s & 3u));
+            if (s & 4u) L.c47 += inc; else L.c03 += inc;
+            ++L.since;
+        }
+        return;
+    }
     L.cur = pay ? (L.cur | (s << 4)) : s;
     if (!L.pend) {
         L.acc |= (uint64_t)L.cur << (8 * L.k);
@@ -176,7 +197,8 @@ __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
 }
 
 __device__ __forceinline__ void lane_finish(Lane& L, const Plan& P, bool failed, bool entropy) {
-    if (L.k > 0) L.outp[L.g4] = L.acc;
+    if (P.op_counts) lane_flush_counts(L, P.op_counts);
+    else if (L.k > 0) L.outp[L.g4] = L.acc;
     csv_stream_result r;
     r.n_entries = L.g4 * 8 + L.k;
     r.flags = 0;
@@ -198,7 +220,7 @@ __device__ __forceinline__ void lane_finish(Lane& L, const Plan& P, bool failed,
 }
 
 // Initialise lane for work item `item`; returns false if the item finished at once.
-template <bool ENTROPY>
+template <bool ENTROPY, bool COUNT>
 __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t item) {
     uint64_t r = item < P.n ? item : item - P.n;
     int s = item < P.n ? 1 : 0;           // detail streams first (longest chains)
@@ -208,10 +230,11 @@ __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t ite
     L.x = 0; L.pos = 0; L.len = 0; L.nb = 0; L.buf = 0;
     uint64_t b = req_local(V, P, r);
     int t = req_lod(P, r);
-    L.outp = reinterpret_cast<uint64_t*>(P.entries + P.eoff[w]);
+    L.c03 = 0; L.c47 = 0; L.since = 0;
+    L.outp = COUNT ? nullptr : reinterpret_cast<uint64_t*>(P.entries + P.eoff[w]);
     bool ok = b < V.nb && t < V.N && !(s == 1 && t != 0);
     L.n = ok ? eff_nibbles(V, b, s) : 0;
-    L.lim = ok ? stream_limit(V, b, t, s) : 0;
+    L.lim = ok ? (COUNT ? L.n : stream_limit(V, b, t, s)) : 0;
     L.tsel = s;
     if (!ok) {
         L.n = 0; L.lim = 0;
@@ -250,7 +273,7 @@ __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t ite
 }
 
 // One symbol; returns false when the lane's item is finished.
-template <bool ENTROPY>
+template <bool ENTROPY, bool COUNT>
 __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t* tab) {
     uint32_t s;
     if (ENTROPY) {
@@ -288,7 +311,7 @@ __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t
     } else {
         s = (L.rawp[L.i >> 1] >> (4 * (L.i & 1))) & 15u;
     }
-    lane_emit(L, s);
+    lane_emit<COUNT>(L, s);
     if (++L.i == L.lim) {
         lane_finish(L, P, false, ENTROPY);
         return false;
@@ -296,7 +319,7 @@ __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t
     return true;
 }
 
-template <bool ENTROPY>
+template <bool ENTROPY, bool COUNT>
 #ifndef K1_MINB
 #define K1_MINB 5
 #endif
@@ -321,7 +344,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MINB) k1_streams(VolView V, Pla
             base = __shfl_sync(FULL, base, leader);
             if (need) {
                 uint64_t my = base + __popc(m & ((1u << lane) - 1u));
-                if (my < total) has = lane_init<ENTROPY>(L, V, P, my);
+                if (my < total) has = lane_init<ENTROPY, COUNT>(L, V, P, my);
                 else done = true;
             }
         }
@@ -329,8 +352,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MINB) k1_streams(VolView V, Pla
         if (has) {
 #pragma unroll 4
             for (int u = 0; u < 32; ++u) {
-                if (!lane_step<ENTROPY>(L, P, tab)) { has = false; break; }
+                if (!lane_step<ENTROPY, COUNT>(L, P, tab)) { has = false; break; }
             }
+            if (COUNT && has && L.since > 16000u) lane_flush_counts(L, P.op_counts);
         }
     }
 }
@@ -837,7 +861,7 @@ __global__ void k_root_raster(VolView V, Plan P) {
 }
 
 // ============================================================================ host launchers
-template <bool E>
+template <bool E, bool COUNT = false>
 static void launch_k1(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
     uint64_t items = 2 * P.n;
     uint64_t want = (items + 31) / 32;                 // warps needed at one item per lane
@@ -845,7 +869,7 @@ static void launch_k1(const VolView& V, const Plan& P, unsigned long long* count
     uint64_t cap = (uint64_t)nsm * 8;                  // 8 x 256 threads per SM resident (32 KB smem each)
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k1_streams<E><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
+    k1_streams<E, COUNT><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
 }
 
 }  // namespace csv
@@ -931,6 +955,15 @@ cudaError_t run_root_raster(const VolView& V, Plan P, cudaStream_t st) {
     unsigned nb = (unsigned)((V.nb + 255) / 256);
     if (nb == 0) return cudaSuccess;
     k_root_raster<<<nb, 256, 0, st>>>(V, P);
+    return cudaGetLastError();
+}
+
+// stats(): K1 in count mode over every brick of the volume (no entry stores)
+cudaError_t run_op_counts(const VolView& V, Plan P, unsigned long long* counter, int nsm, cudaStream_t st) {
+    if (P.n == 0) return cudaSuccess;
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    if (V.entropy) launch_k1<true, true>(V, P, counter, nsm, st);
+    else launch_k1<false, true>(V, P, counter, nsm, st);
     return cudaGetLastError();
 }
 

@@ -54,6 +54,7 @@ struct Plan {
     csv_stream_result* sres;   // [2n]
     uint8_t* entries;
     csv_result* res;           // [n] or nullptr
+    unsigned long long* op_counts;   // K1 count mode (stats): 8 per-op totals, else nullptr
 };
 
 __device__ __forceinline__ uint64_t req_local(const VolView& V, const Plan& P, uint64_t r) {

@@ -185,6 +185,16 @@ class GpuVolume:
                                             _ptr(offs), _ptr(sres), _stream_handle(torch, stream)))
         return entries, offs, sres
 
+    def op_counts(self, stream=None):
+        """K1 in count mode: (per-op totals int64[8], per-stream results [2n] structured)."""
+        torch = self._torch
+        n = self.n_bricks
+        counts = torch.zeros(8, dtype=torch.int64, device=self.device)
+        sres = torch.zeros((max(2 * n, 1), 4), dtype=torch.int32, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().csv_volume_op_counts(self._h, _ptr(counts), _ptr(sres), _stream_handle(torch, stream)))
+        return counts.cpu().numpy(), sres[: 2 * n].cpu().numpy().view(_lib.STREAM_RESULT_DTYPE).reshape(2 * n)
+
     def set_timing(self, enable: bool = True) -> None:
         _lib.check(_lib.lib().csv_volume_set_timing(self._h, 1 if enable else 0))
 

@@ -231,5 +231,22 @@ def main():
     print("config1", cfg["input_sha"], cfg["container_sha"], len(data))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("CSV_GOLDEN_STATS"):
     sys.exit(main())
+
+
+def make_stats_goldens():
+    """stats() of the reference for a few golden containers."""
+    out = {}
+    for name in ("a_b3", "d_b5_mem", "e_b4_raw", "f_b2_noise", "i_const", "g_b6"):
+        with open(os.path.join(OUT, f"vol_{name}.csv1"), "rb") as f:
+            c = csvol.CsvContainer.from_bytes(f.read())
+        out[name] = cvol.stats(c)
+    with open(os.path.join(OUT, "config1.csv1"), "rb") as f:
+        out["config1"] = cvol.stats(csvol.CsvContainer.from_bytes(f.read()))
+    with open(os.path.join(OUT, "stats.json"), "w") as f:
+        json.dump(out, f, indent=1, default=lambda o: list(o) if isinstance(o, tuple) else o)
+
+
+if __name__ == "__main__" and os.environ.get("CSV_GOLDEN_STATS"):
+    make_stats_goldens()

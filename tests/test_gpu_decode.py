@@ -141,3 +141,27 @@ def test_slab_partition_equals_whole(pkg):
         vol = c.to_device(brick_range=(z0 * gx * gy, z1 * gx * gy))
         parts.append(pkg.decompress_volume_device(vol, 0).cpu().numpy().view(np.uint32))
     assert np.array_equal(np.concatenate(parts, axis=0), full)
+
+
+@pytest.mark.parametrize("name", ["a_b3", "d_b5_mem", "e_b4_raw", "f_b2_noise", "i_const", "g_b6", "config1"])
+def test_stats_matches_reference(pkg, name):
+    """stats() (op histogram from K1 count mode) == the reference's stats() output."""
+    import json
+    exp = golden_json("stats.json")[name]
+    path = GOLDEN + ("/config1.csv1" if name == "config1" else f"/vol_{name}.csv1")
+    with open(path, "rb") as f:
+        c = pkg.CsvContainer.from_bytes(f.read())
+    got = json.loads(json.dumps(pkg.stats(c)))
+    assert got == exp
+
+
+def test_stats_errors_match_rans_decode(pkg):
+    """Corrupted streams raise rans_decode's messages (rans.py:192-197)."""
+    with open(GOLDEN + "/vol_d_b5_mem.csv1", "rb") as f:
+        data = bytearray(f.read())
+    c = pkg.CsvContainer.from_bytes(bytes(data))
+    d = c.directory.copy()
+    d[3]["detail_bytes"] -= 3          # truncated detail stream of brick 3
+    c.directory = d
+    with pytest.raises(pkg.CorruptStreamError, match="entropy stream (truncated at symbol|desynchronized)"):
+        pkg.stats(c)
