@@ -115,6 +115,12 @@ int csv_volume_free(csv_volume* vol);
 int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, int64_t z_end,
                       csv_result* d_res, uintptr_t stream);
 
+/* Same for the bricks [brick_first, brick_last) (global indices inside the
+ * volume's range) only: the unit of the slab pipeline that overlaps decode with
+ * device-to-host copies.  d_res receives brick_last - brick_first results. */
+int csv_decode_volume_range(csv_volume* vol, int t, uint64_t brick_first, uint64_t brick_last, uint32_t* d_out,
+                            int64_t z_begin, int64_t z_end, csv_result* d_res, uintptr_t stream);
+
 /* Batched random-access decode into a Morton-order brick pool: replaces the
  * per-brick CsvContainer.decode_brick (container.py:168-208) loop inside
  * BrickCache._store / end_frame_assign (cache.py:125-170).  Request i decodes

@@ -308,19 +308,61 @@ def decompress_volume_device(container, t: int = 0, out=None, z_range=None, stre
     return out
 
 
-def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None = None, out: np.ndarray | None = None):
+def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None = None, out: np.ndarray | None = None,
+                      slab_layers: int | None = None):
     """Reassemble the volume at LOD t, cropped to ceil(dims / 2**t) (container.py:456-478).
 
-    ``workers`` is accepted for signature compatibility; the decode is a
-    single batched GPU launch.  ``out`` may be a preallocated (ideally
-    pinned) uint32 host array of the cropped shape.
+    ``workers`` is accepted for signature compatibility.  The decode runs on the
+    GPU in slabs of whole bz layers, double-buffered so that each slab's
+    device-to-host copy overlaps the next slab's decode.  ``out`` may be a
+    preallocated (ideally pinned) uint32 host array of the cropped shape.
     """
-    _check_t(container.meta, t)
-    dev = decompress_volume_device(container, t)
-    if out is None:
-        return dev.cpu().numpy().view(np.uint32)
     import torch
-    torch.from_numpy(out.view(np.int32)).copy_(dev)
+    from .device import GpuVolume
+    _check_t(container.meta, t)
+    meta = container.meta
+    x, y, z = meta.dims
+    cz, cy, cx = (-(-d // (1 << t)) for d in (z, y, x))
+    if out is None:
+        out = np.empty((cz, cy, cx), dtype=np.uint32)
+    elif out.shape != (cz, cy, cx) or out.dtype != np.uint32:
+        raise ValueError(f"out must be a uint32 array of shape {(cz, cy, cx)}")
+    vol = container.to_device()
+    try:
+        n = vol.n_bricks
+        dev = vol.device
+        gx, gy, gz = meta.grid_dims
+        side = meta.brick_side >> t
+        if slab_layers is None:
+            slab_layers = max(1, -(-gz // 8))
+        layer = gx * gy
+        results = torch.empty((max(n, 1), 4), dtype=torch.int64, device=dev)
+        host = torch.from_numpy(out.view(np.int32))
+        rows = min(slab_layers * side, cz)
+        bufs = [torch.empty((rows, cy, cx), dtype=torch.int32, device=dev) for _ in range(2 if gz > slab_layers else 1)]
+        comp = torch.cuda.current_stream(dev)
+        copy = torch.cuda.Stream(dev)
+        freed = [torch.cuda.Event() for _ in bufs]
+        ready = [torch.cuda.Event() for _ in bufs]
+        for k, bz0 in enumerate(range(0, gz, slab_layers)):
+            bz1 = min(bz0 + slab_layers, gz)
+            z0, z1 = min(bz0 * side, cz), min(bz1 * side, cz)
+            i = k % len(bufs)
+            if k >= len(bufs):
+                comp.wait_event(freed[i])
+            vol.decode_range(t, bz0 * layer, bz1 * layer, bufs[i], (z0, z1), results[bz0 * layer:], stream=comp)
+            ready[i].record(comp)
+            copy.wait_event(ready[i])
+            with torch.cuda.stream(copy):
+                host[z0:z1].copy_(bufs[i][: z1 - z0], non_blocking=True)
+            freed[i].record(copy)
+        copy.synchronize()
+        torch.cuda.synchronize(dev)
+        if t == meta.brick_log2 and n and bool((results[:n, 0] & 0xFFFFFFFF).eq(8).any()):
+            raise ValueError("expected 1 entries, got shape (0,)")   # morton_to_grid on an empty palette[:1]
+        GpuVolume.raise_first(results, n)
+    finally:
+        vol.close()
     return out
 
 

@@ -331,14 +331,17 @@ int csv_volume_info(csv_volume* vol, int64_t* dims3, int64_t* grid3, int* brick_
     return CSV_OK;
 }
 
-int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, int64_t z_end, csv_result* d_res,
-                      uintptr_t stream) {
+int csv_decode_volume_range(csv_volume* vol, int t, uint64_t brick_first, uint64_t brick_last, uint32_t* d_out,
+                            int64_t z_begin, int64_t z_end, csv_result* d_res, uintptr_t stream) {
     if (!vol || !d_out) return fail(CSV_E_ARG, "null argument");
     if (t < 0 || t > vol->V.N) return fail(CSV_E_ARG, "LOD %d outside [0, %d]", t, vol->V.N);
+    if (brick_first < vol->V.brick_begin || brick_last > vol->V.brick_begin + vol->V.nb || brick_last < brick_first)
+        return fail(CSV_E_ARG, "brick range outside the volume");
     CUDA_TRY(cudaSetDevice(vol->device));
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Plan P{};
-    P.n = vol->V.nb;
+    P.n = brick_last - brick_first;
+    P.first = brick_first - vol->V.brick_begin;
     P.t_uniform = t;
     P.out = d_out;
     P.z_begin = z_begin;
@@ -346,6 +349,7 @@ int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, 
     P.cx = (vol->dims[0] + (1ll << t) - 1) >> t;
     P.cy = (vol->dims[1] + (1ll << t) - 1) >> t;
     P.res = d_res;
+    if (P.n == 0) return CSV_OK;
     if (t == vol->V.N) {
         CUDA_TRY(csv::run_root_raster(vol->V, P, st));
         return CSV_OK;
@@ -358,6 +362,13 @@ int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, 
     CUDA_TRY(run_decode(vol->V, P, 0, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
                         vol->gws_ctas, vol->nsm, t, st, vol->timing ? vol->ev : nullptr));
     return CSV_OK;
+}
+
+int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, int64_t z_end, csv_result* d_res,
+                      uintptr_t stream) {
+    if (!vol) return fail(CSV_E_ARG, "null volume");
+    return csv_decode_volume_range(vol, t, vol->V.brick_begin, vol->V.brick_begin + vol->V.nb, d_out, z_begin, z_end,
+                                   d_res, stream);
 }
 
 int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, const uint8_t* d_lod,

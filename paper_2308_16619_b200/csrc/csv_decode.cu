@@ -846,12 +846,14 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
 
 // Coarsest-LOD raster (t == N): one voxel per brick.
 __global__ void k_root_raster(VolView V, Plan P) {
-    uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= P.n) return;
+    uint64_t b = P.first + r;
     if (b >= V.nb) return;
     uint32_t plen = V.pal_len[b];
     if (P.res) {
         csv_result o{plen == 0 ? CSV_ST_EMPTY_PALETTE : 0, 0, 0, 0, 0};
-        P.res[b] = o;
+        P.res[r] = o;
     }
     if (plen == 0) return;
     uint64_t gb = V.brick_begin + b;
@@ -952,7 +954,7 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
 }
 
 cudaError_t run_root_raster(const VolView& V, Plan P, cudaStream_t st) {
-    unsigned nb = (unsigned)((V.nb + 255) / 256);
+    unsigned nb = (unsigned)((P.n + 255) / 256);
     if (nb == 0) return cudaSuccess;
     k_root_raster<<<nb, 256, 0, st>>>(V, P);
     return cudaGetLastError();

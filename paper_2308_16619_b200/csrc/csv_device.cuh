@@ -43,7 +43,8 @@ struct VolView {
 // One decode call: n requests; request r decodes brick `brick[r]` at LOD lod[r].
 struct Plan {
     uint64_t n;
-    const uint32_t* brick;     // global brick index, or nullptr => brick_begin + r
+    uint64_t first;            // implicit requests: local brick first + r
+    const uint32_t* brick;     // global brick index, or nullptr => brick_begin + first + r
     const uint8_t* lod;        // per-request LOD, or nullptr => t_uniform
     int t_uniform;
     const uint64_t* dst;       // Morton mode: pool element offset per request
@@ -58,7 +59,7 @@ struct Plan {
 };
 
 __device__ __forceinline__ uint64_t req_local(const VolView& V, const Plan& P, uint64_t r) {
-    return P.brick ? (uint64_t)P.brick[r] - V.brick_begin : r;
+    return P.brick ? (uint64_t)P.brick[r] - V.brick_begin : P.first + r;
 }
 __device__ __forceinline__ int req_lod(const Plan& P, uint64_t r) {
     return P.lod ? (int)P.lod[r] : P.t_uniform;

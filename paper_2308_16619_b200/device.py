@@ -159,6 +159,15 @@ class GpuVolume:
                                                     _stream_handle(torch, stream)))
         return out, results
 
+    def decode_range(self, t: int, brick_first: int, brick_last: int, out, z_range, results, stream=None):
+        """Raster decode of bricks [brick_first, brick_last) into the z-slab `out` (rows z_range)."""
+        torch = self._torch
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().csv_decode_volume_range(self._h, t, brick_first, brick_last, _ptr(out),
+                                                          z_range[0], z_range[1], _ptr(results),
+                                                          _stream_handle(torch, stream)))
+        return out
+
     def decode_bricks(self, bricks, lods, dst, pool, results=None, stream=None):
         """Batched Morton decode (K1 + K2/K4) of (brick, lod) requests into pool[dst:...]."""
         torch = self._torch
