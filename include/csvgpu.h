@@ -104,6 +104,16 @@ int csv_volume_create_device(int device, const uint8_t* head120, const uint8_t* 
                              const uint8_t* d_detail, uint64_t detail_base, uint64_t detail_len,
                              uintptr_t stream, csv_volume** vol);
 
+/* Deferred upload: the directory and tables are uploaded now, the three blob
+ * slices are allocated but filled later with csv_volume_upload (blob 0 palette,
+ * 1 coarse, 2 detail; offset/nbytes in bytes relative to the slice), so a host
+ * pipeline can overlap uploading slab k+1 with decoding slab k. */
+int csv_volume_create_deferred(int device, const uint8_t* head120, const uint8_t* dir44, uint64_t brick_begin,
+                               uint64_t brick_end, uint64_t palette_base, uint64_t palette_len, uint64_t coarse_base,
+                               uint64_t coarse_len, uint64_t detail_base, uint64_t detail_len, uintptr_t stream,
+                               csv_volume** vol);
+int csv_volume_upload(csv_volume* vol, int blob, const void* host, uint64_t offset, uint64_t nbytes, uintptr_t stream);
+
 int csv_volume_free(csv_volume* vol);
 
 /* Full-volume decode at LOD t into a raster (Z,Y,X) u32 slab: replaces

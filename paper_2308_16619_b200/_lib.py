@@ -24,7 +24,7 @@ EXPORTS = (
     "csv_decode_volume", "csv_decode_bricks", "csv_decode_streams", "csv_streams_capacity", "csv_volume_info",
     "csv_encode_volume", "csv_encoded_info", "csv_encoded_device_ptrs", "csv_encoded_copy_to_host",
     "csv_encoded_free", "csv_synth_voronoi", "csv_volume_set_timing", "csv_volume_get_timing",
-    "csv_volume_op_counts", "csv_decode_volume_range",
+    "csv_volume_op_counts", "csv_decode_volume_range", "csv_volume_create_deferred", "csv_volume_upload",
 )
 
 
@@ -77,6 +77,10 @@ def lib():
         L.csv_encoded_free.argtypes = [P]
         L.csv_synth_voronoi.restype = I
         L.csv_synth_voronoi.argtypes = [P, I64, I64, I64, I, ctypes.c_uint32, I, ctypes.c_double, ctypes.c_uint32, UP]
+        L.csv_volume_create_deferred.restype = I
+        L.csv_volume_create_deferred.argtypes = [I, P, P, U64, U64, U64, U64, U64, U64, U64, U64, UP, P]
+        L.csv_volume_upload.restype = I
+        L.csv_volume_upload.argtypes = [P, I, P, U64, U64, UP]
         L.csv_decode_volume_range.restype = I
         L.csv_decode_volume_range.argtypes = [P, I, U64, U64, P, I64, I64, P, UP]
         L.csv_volume_op_counts.restype = I

@@ -327,7 +327,20 @@ def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None =
         out = np.empty((cz, cy, cx), dtype=np.uint32)
     elif out.shape != (cz, cy, cx) or out.dtype != np.uint32:
         raise ValueError(f"out must be a uint32 array of shape {(cz, cy, cx)}")
-    vol = container.to_device()
+    if container.detail_blob is None:
+        raise ConfigError("device upload needs the detail section in memory")
+    # three-stage pipeline per slab of whole bz layers: upload its compressed
+    # bytes (blobs are in brick order, container.py:428-445) -> decode -> D2H
+    d = container.directory
+    blobs = (container.palette_blob.astype("<u4", copy=False).view(np.uint8), container.coarse_blob,
+             container.detail_blob)
+    ends = []
+    for k, (ocol, lcol, scale) in enumerate((("palette_off", "palette_len", 4), ("coarse_off", "coarse_bytes", 1),
+                                              ("detail_off", "detail_bytes", 1))):
+        e = (d[ocol].astype(np.int64) + d[lcol].astype(np.int64)) * scale
+        ends.append(np.minimum(np.maximum.accumulate(e), blobs[k].size) if e.size else e)
+    vol = GpuVolume(container.head_bytes(), d, container.palette_blob.size, container.coarse_blob.size,
+                    container.detail_blob.size, deferred=True)
     try:
         n = vol.n_bricks
         dev = vol.device
@@ -341,22 +354,47 @@ def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None =
         rows = min(slab_layers * side, cz)
         bufs = [torch.empty((rows, cy, cx), dtype=torch.int32, device=dev) for _ in range(2 if gz > slab_layers else 1)]
         comp = torch.cuda.current_stream(dev)
-        copy = torch.cuda.Stream(dev)
+        up = torch.cuda.Stream(dev)
+        copies = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
         freed = [torch.cuda.Event() for _ in bufs]
         ready = [torch.cuda.Event() for _ in bufs]
-        for k, bz0 in enumerate(range(0, gz, slab_layers)):
+        uploaded = [0, 0, 0]
+        slabs = list(range(0, gz, slab_layers))
+
+        def upload_until(bz1):
+            last = min(bz1 * layer, n) - 1
+            for k in range(3):
+                hi = int(ends[k][last]) if last >= 0 else 0
+                if hi > uploaded[k]:
+                    vol.upload(k, blobs[k][uploaded[k]:hi], uploaded[k], stream=up)
+                    uploaded[k] = hi
+            ev = torch.cuda.Event()
+            ev.record(up)
+            return ev
+
+        up_ev = upload_until(min(slab_layers, gz))
+        for k, bz0 in enumerate(slabs):
             bz1 = min(bz0 + slab_layers, gz)
             z0, z1 = min(bz0 * side, cz), min(bz1 * side, cz)
             i = k % len(bufs)
+            comp.wait_event(up_ev)
             if k >= len(bufs):
                 comp.wait_event(freed[i])
             vol.decode_range(t, bz0 * layer, bz1 * layer, bufs[i], (z0, z1), results[bz0 * layer:], stream=comp)
             ready[i].record(comp)
-            copy.wait_event(ready[i])
-            with torch.cuda.stream(copy):
-                host[z0:z1].copy_(bufs[i][: z1 - z0], non_blocking=True)
-            freed[i].record(copy)
-        copy.synchronize()
+            half = (z1 - z0 + 1) // 2
+            for h, (a, b) in enumerate(((z0, z0 + half), (z0 + half, z1))):
+                if b > a:
+                    copies[h].wait_event(ready[i])
+                    with torch.cuda.stream(copies[h]):
+                        host[a:b].copy_(bufs[i][a - z0: b - z0], non_blocking=True)
+            fe = freed[i]
+            fe.record(copies[0])
+            comp.wait_stream(copies[1])  # keep the second half ordered before the buffer's reuse
+            if k + 1 < len(slabs):
+                up_ev = upload_until(min(slabs[k + 1] + slab_layers, gz))
+        for s_ in copies:
+            s_.synchronize()
         torch.cuda.synchronize(dev)
         if t == meta.brick_log2 and n and bool((results[:n, 0] & 0xFFFFFFFF).eq(8).any()):
             raise ValueError("expected 1 entries, got shape (0,)")   # morton_to_grid on an empty palette[:1]

@@ -67,6 +67,7 @@ struct csv_volume {
     uint64_t region_total_t0 = 0;   // sum over bricks of entry regions at t=0 (bytes)
     uint64_t region_max_t0 = 0;     // max over bricks
     int64_t dims[3]{}, grid[3]{};
+    uint64_t blob_cap[3]{};         // bytes of the palette / coarse / detail slices held
     bool timing = false;
     cudaEvent_t ev[4]{};            // plan start, K1 start, K1 end / K2 start, K2 end
 };
@@ -207,7 +208,7 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
                       const uint32_t* palette, uint64_t palette_base, uint64_t palette_len,
                       const uint8_t* coarse, uint64_t coarse_base, uint64_t coarse_len,
                       const uint8_t* detail, uint64_t detail_base, uint64_t detail_len,
-                      bool blobs_on_device, uintptr_t stream, csv_volume** out) {
+                      bool blobs_on_device, uintptr_t stream, csv_volume** out, bool deferred = false) {
     if (!head120 || !out) return fail(CSV_E_ARG, "null argument");
     if (brick_end < brick_begin) return fail(CSV_E_ARG, "brick_end < brick_begin");
     CUDA_TRY(cudaSetDevice(device));
@@ -254,9 +255,12 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
         ce = cudaMalloc(&v->d_blob, pb + cb + db);
         if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "blobs: %s", cudaGetErrorString(ce)); }
         cudaMemsetAsync(v->d_blob, 0, pb + cb + db, st);
-        if (palette_len) cudaMemcpyAsync(v->d_blob, palette, palette_len * 4, cudaMemcpyHostToDevice, st);
-        if (coarse_len) cudaMemcpyAsync(v->d_blob + pb, coarse, coarse_len, cudaMemcpyHostToDevice, st);
-        if (detail_len) cudaMemcpyAsync(v->d_blob + pb + cb, detail, detail_len, cudaMemcpyHostToDevice, st);
+        if (!deferred) {
+            if (palette_len) cudaMemcpyAsync(v->d_blob, palette, palette_len * 4, cudaMemcpyHostToDevice, st);
+            if (coarse_len) cudaMemcpyAsync(v->d_blob + pb, coarse, coarse_len, cudaMemcpyHostToDevice, st);
+            if (detail_len) cudaMemcpyAsync(v->d_blob + pb + cb, detail, detail_len, cudaMemcpyHostToDevice, st);
+        }
+        v->blob_cap[0] = palette_len * 4; v->blob_cap[1] = coarse_len; v->blob_cap[2] = detail_len;
         v->V.palette = (const uint32_t*)v->d_blob;
         v->V.coarse = v->d_blob + pb;
         v->V.detail = v->d_blob + pb + cb;
@@ -290,6 +294,10 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
         v->region_total_t0 = hs[0];
         v->region_max_t0 = hs[1];
     }
+    if (deferred) {  // the zero fill must land before uploads issued on other streams
+        ce = cudaStreamSynchronize(st);
+        if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_CUDA, "create: %s", cudaGetErrorString(ce)); }
+    }
     *out = v;
     return CSV_OK;
 }
@@ -315,6 +323,25 @@ int csv_volume_create_device(int device, const uint8_t* head120, const uint8_t* 
                              uint64_t detail_len, uintptr_t stream, csv_volume** vol) {
     return vol_create(device, head120, d_dir44, true, brick_begin, brick_end, d_palette, palette_base, palette_len,
                       d_coarse, coarse_base, coarse_len, d_detail, detail_base, detail_len, true, stream, vol);
+}
+
+int csv_volume_create_deferred(int device, const uint8_t* head120, const uint8_t* dir44, uint64_t brick_begin,
+                               uint64_t brick_end, uint64_t palette_base, uint64_t palette_len, uint64_t coarse_base,
+                               uint64_t coarse_len, uint64_t detail_base, uint64_t detail_len, uintptr_t stream,
+                               csv_volume** vol) {
+    return vol_create(device, head120, dir44, false, brick_begin, brick_end, nullptr, palette_base, palette_len,
+                      nullptr, coarse_base, coarse_len, nullptr, detail_base, detail_len, false, stream, vol, true);
+}
+
+int csv_volume_upload(csv_volume* vol, int blob, const void* host, uint64_t offset, uint64_t nbytes, uintptr_t stream) {
+    if (!vol || blob < 0 || blob > 2 || (nbytes && !host)) return fail(CSV_E_ARG, "bad upload arguments");
+    if (!vol->d_blob) return fail(CSV_E_ARG, "volume does not own its blobs");
+    if (offset + nbytes > vol->blob_cap[blob]) return fail(CSV_E_ARG, "upload beyond the blob slice");
+    if (nbytes == 0) return CSV_OK;
+    CUDA_TRY(cudaSetDevice(vol->device));
+    uint8_t* base = blob == 0 ? (uint8_t*)vol->V.palette : (blob == 1 ? (uint8_t*)vol->V.coarse : (uint8_t*)vol->V.detail);
+    CUDA_TRY(cudaMemcpyAsync(base + offset, host, nbytes, cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream)));
+    return CSV_OK;
 }
 
 int csv_volume_free(csv_volume* vol) {

@@ -63,7 +63,7 @@ class GpuVolume:
     def __init__(self, head120: bytes, directory: np.ndarray, palette, coarse, detail,
                  brick_begin: int = 0, brick_end: int | None = None,
                  palette_base: int = 0, coarse_base: int = 0, detail_base: int = 0,
-                 device=None, stream=None, on_device: bool = False):
+                 device=None, stream=None, on_device: bool = False, deferred: bool = False):
         torch = _lib.require_cuda()
         self._torch = torch
         L = _lib.lib()
@@ -91,6 +91,14 @@ class GpuVolume:
                 rc = L.csv_volume_create_device(
                     self.device.index, _ptr(head), dp, self.brick_begin, self.brick_end,
                     pp, palette_base, pn, cp, coarse_base, cn, xp, detail_base, xn, sh, ctypes.byref(handle))
+            elif deferred:
+                # blobs allocated now, filled by upload(); palette/coarse/detail are their lengths
+                d = np.ascontiguousarray(directory).view(np.uint8)
+                self._keep = (head120, d)
+                rc = L.csv_volume_create_deferred(
+                    self.device.index, _ptr(head), _ptr(d), self.brick_begin, self.brick_end,
+                    palette_base, int(palette), coarse_base, int(coarse), detail_base, int(detail), sh,
+                    ctypes.byref(handle))
             else:
                 d = np.ascontiguousarray(directory).view(np.uint8)
                 pal = np.ascontiguousarray(palette, dtype="<u4")
@@ -158,6 +166,13 @@ class GpuVolume:
             _lib.check(_lib.lib().csv_decode_volume(self._h, t, _ptr(out), z0, z1, _ptr(results),
                                                     _stream_handle(torch, stream)))
         return out, results
+
+    def upload(self, blob: int, host: np.ndarray, offset: int, stream=None) -> None:
+        """Fill bytes [offset, offset + host.nbytes) of blob 0 palette / 1 coarse / 2 detail (deferred volumes)."""
+        torch = self._torch
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().csv_volume_upload(self._h, blob, _ptr(host), offset, host.nbytes,
+                                                    _stream_handle(torch, stream)))
 
     def decode_range(self, t: int, brick_first: int, brick_last: int, out, z_range, results, stream=None):
         """Raster decode of bricks [brick_first, brick_last) into the z-slab `out` (rows z_range)."""
