@@ -119,8 +119,9 @@ int csv_volume_free(csv_volume* vol);
 /* Full-volume decode at LOD t into a raster (Z,Y,X) u32 slab: replaces
  * decompress_volume (container.py:456-478) + morton_to_grid (morton.py:411-416).
  * d_out holds LOD-t z rows [z_begin, z_end) of the volume cropped to
- * ceil(dims / 2^t) (container.py:476-478); only this volume's bricks are
- * decoded.  d_res (may be NULL) receives one csv_result per brick of the
+ * ceil(dims / 2^t) (container.py:476-478); z_begin must be a multiple of the
+ * LOD-t brick side (2^(brick_log2 - t)), else CSV_E_ARG; only this volume's
+ * bricks are decoded.  d_res (may be NULL) receives one csv_result per brick of the
  * volume's range, in brick order. */
 int csv_decode_volume(csv_volume* vol, int t, uint32_t* d_out, int64_t z_begin, int64_t z_end,
                       csv_result* d_res, uintptr_t stream);

@@ -13,7 +13,7 @@ import subprocess
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcsvgpu.so")
+LIB_PATH = os.environ.get("CSVGPU_LIB") or os.path.join(_PKG, "libcsvgpu.so")   # override: build variants
 _lib = None
 
 RESULT_DTYPE = np.dtype([("status", "<i4"), ("stream", "<i4"), ("pos", "<i8"), ("ci", "<i8"), ("di", "<i8")])

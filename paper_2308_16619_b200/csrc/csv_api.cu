@@ -364,6 +364,9 @@ int csv_decode_volume_range(csv_volume* vol, int t, uint64_t brick_first, uint64
     if (t < 0 || t > vol->V.N) return fail(CSV_E_ARG, "LOD %d outside [0, %d]", t, vol->V.N);
     if (brick_first < vol->V.brick_begin || brick_last > vol->V.brick_begin + vol->V.nb || brick_last < brick_first)
         return fail(CSV_E_ARG, "brick range outside the volume");
+    if (z_begin < 0 || z_end < z_begin || z_begin % (1ll << (vol->V.N - t)) != 0)
+        return fail(CSV_E_ARG, "z range [%lld, %lld) must start on a brick boundary (multiple of %lld)",
+                    (long long)z_begin, (long long)z_end, 1ll << (vol->V.N - t));
     CUDA_TRY(cudaSetDevice(vol->device));
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Plan P{};

@@ -27,8 +27,11 @@ __device__ __forceinline__ uint32_t nth_set_bit(uint32_t m, uint32_t r) {
     return pos;
 }
 
+#ifndef K2F_MINB
+#define K2F_MINB 5
+#endif
 template <int MODE, int LMAX>
-__global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
+__global__ void __launch_bounds__(K2_THREADS, K2F_MINB) k2_fast(VolView V, Plan P) {
     static_assert(LMAX <= 5, "shared-memory replay covers N - t <= 5");
     constexpr Layout Y = make_layout(LMAX, 2);
     extern __shared__ __align__(16) uint32_t dsm[];
@@ -78,6 +81,10 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
     }
     const csv_stream_result src = P.sres[2 * r], srd = P.sres[2 * r + 1];
     const uint64_t eo0 = P.eoff[2 * r], eo1 = P.eoff[2 * r + 1], eo2 = P.eoff[2 * r + 2];
+    if (threadIdx.x == 0 && eo2 > eo0) {   // stage this brick's entries in L2 ahead of the level loop
+        const uint64_t lo = eo0 & ~15ull, hi = (eo2 + 15) & ~15ull;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(P.entries + lo), "r"((uint32_t)(hi - lo)) : "memory");
+    }
     const bool trivial = (uint64_t)nc + nd == 0;     // relevant == 0: fill palette[0] (codec.py:353-358)
     if (threadIdx.x == 0) {
         dsm[Y.lev] = __ldg(pal);      // root (codec.py:353)
@@ -393,7 +400,34 @@ __global__ void __launch_bounds__(K2_THREADS, 5) k2_fast(VolView V, Plan P) {
                         if (!((dsm[Y.pend + (cl >> 5)] >> (cl & 31)) & 1u)) break;
                     }
                     uint32_t* d = child_ptr(j);
-                    if (d) *d = *child_ptr(cl);
+                    if (!d) continue;
+                    if (!final_level) { *d = clev[cl]; continue; }
+                    // final level: evaluate the chain's end child cl from shared state
+                    // instead of reading back the output it was stored to
+                    const uint32_t qc = cl >> 3, cc = cl & 7u;
+                    const uint32_t mwc = pmask[qc >> 5];
+                    uint32_t val = plev[qc];
+                    if ((mwc >> (qc & 31)) & 1u) {
+                        const uint32_t rkc = dsm[Y.wpre + (qc >> 5)] + __popc(mwc & ((1u << (qc & 31)) - 1u));
+                        const uint32_t ec0 = e0 + 8 * rkc;
+                        const uint64_t wc = ec0 + 8 <= ecap ? __ldg(reinterpret_cast<const uint64_t*>(Eb + ec0)) : 0ull;
+                        const uint32_t e = (uint32_t)(wc >> (8 * cc)) & 0xFFu;
+                        const uint32_t op = e & 7u;
+                        const uint32_t a = op - 1u;
+                        if (a < 3u) {   // not pending: odd -> +1 parent, even -> inactive -1 parent
+                            const uint32_t M = a == 0 ? Mx : (a == 1 ? My : Mz);
+                            const uint32_t part = cl & M, rest = cl & ~M;
+                            const uint32_t nb = (cc >> a) & 1u ? ((((part | ~M) + 1u) & M) | rest)
+                                                                : (((part - 1u) & M) | rest);
+                            val = plev[nb >> 3];
+                        } else if (op >= 4u && op <= 6u) {
+                            const int32_t ip = ipbase + (int32_t)ipb[rkc] + (int32_t)prefix_bytes(op_eq(wc, 6), cc);
+                            int32_t idx = op == 4u ? ip : (op == 5u ? ip - (int32_t)(e >> 4) - 1 : ip + 1);
+                            idx = min(max(idx, 0), (int32_t)plen - 1);
+                            val = __ldg(pal + idx);
+                        }
+                    }
+                    *d = val;
                 }
             }
         }

@@ -143,6 +143,21 @@ def test_slab_partition_equals_whole(pkg):
     assert np.array_equal(np.concatenate(parts, axis=0), full)
 
 
+def test_z_range_rows(pkg):
+    """z rows [z0, z1) of the full volume; z0 must sit on a brick boundary (chains read lower rows)."""
+    with open(GOLDEN + "/config1.csv1", "rb") as f:
+        c = pkg.CsvContainer.from_bytes(f.read())
+    vol = c.to_device()
+    for t in (0, 1):
+        full = pkg.decompress_volume(c, t)
+        side = c.meta.brick_side >> t
+        z0, z1 = side, min(2 * side + 5, full.shape[0])
+        part = pkg.decompress_volume_device(vol, t, z_range=(z0, z1)).cpu().numpy().view(np.uint32)
+        assert np.array_equal(part, full[z0:z1])
+        with pytest.raises(RuntimeError, match="brick boundary"):
+            pkg.decompress_volume_device(vol, t, z_range=(z0 + 1, z1))
+
+
 @pytest.mark.parametrize("name", ["a_b3", "d_b5_mem", "e_b4_raw", "f_b2_noise", "i_const", "g_b6", "config1"])
 def test_stats_matches_reference(pkg, name):
     """stats() (op histogram from K1 count mode) == the reference's stats() output."""
