@@ -60,6 +60,7 @@ struct csv_volume {
     uint8_t* d_entries = nullptr;
     uint64_t entries_cap = 0;
     uint32_t* d_gws = nullptr;
+    uint16_t* d_wscratch = nullptr;  // K2w per-warp palette bases (nsm x 64 warps x 4096)
     uint64_t gws_stride = 0;
     int gws_ctas = 0;
     uint64_t gws_words_cap = 0;
@@ -105,6 +106,7 @@ __global__ void k_unpack_dir(const uint8_t* dir44, uint64_t n, uint64_t pal_base
 
 __global__ void k_region_stats(VolView V, unsigned long long* total, unsigned long long* mx) {
     uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (b < V.nb) atomicMax(mx + 1, (unsigned long long)V.pal_len[b]);
     unsigned long long s = 0;
     if (b < V.nb && V.N > 0) s = round32(stream_limit(V, b, 0, 0)) + round32(stream_limit(V, b, 0, 1));
     unsigned long long m = s;
@@ -158,7 +160,7 @@ static void vol_release(csv_volume* v) {
     cudaSetDevice(v->device);
     cudaFree(v->d_soa); cudaFree(v->d_blob); cudaFree(v->d_dtab);
     cudaFree(v->d_sizes); cudaFree(v->d_eoff); cudaFree(v->d_scan); cudaFree(v->d_sres);
-    cudaFree(v->d_counter); cudaFree(v->d_entries); cudaFree(v->d_gws);
+    cudaFree(v->d_counter); cudaFree(v->d_entries); cudaFree(v->d_gws); cudaFree(v->d_wscratch);
     for (auto& e : v->ev) if (e) cudaEventDestroy(e);
     delete v;
 }
@@ -173,9 +175,10 @@ static int ensure_plan(csv_volume* v, uint64_t n, uint64_t entries_need, int Lg,
         CUDA_TRY(cudaMalloc(&v->d_sres, 2 * cap * sizeof(csv_stream_result)));
         v->plan_cap = cap;
     }
+    if (!v->d_wscratch) CUDA_TRY(cudaMalloc(&v->d_wscratch, (size_t)v->nsm * 64 * kWScratchStride * sizeof(uint16_t)));
     if (!v->d_scan) {
         CUDA_TRY(cudaMalloc(&v->d_scan, 4104 * sizeof(uint64_t)));
-        CUDA_TRY(cudaMalloc(&v->d_counter, sizeof(unsigned long long)));
+        CUDA_TRY(cudaMalloc(&v->d_counter, 4 * sizeof(unsigned long long)));
     }
     if (entries_need + 64 > v->entries_cap) {
         cudaStreamSynchronize(st);
@@ -282,17 +285,18 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
                                                                coarse_len, detail_base, detail_len, pal_off, pal_n,
                                                                c_off, c_bytes, c_nib, d_off, d_bytes, d_nib);
         unsigned long long* stats = nullptr;
-        cudaMalloc(&stats, 16);
-        cudaMemsetAsync(stats, 0, 16, st);
+        cudaMalloc(&stats, 24);
+        cudaMemsetAsync(stats, 0, 24, st);
         k_region_stats<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v->V, stats, stats + 1);
-        unsigned long long hs[2] = {0, 0};
-        cudaMemcpyAsync(hs, stats, 16, cudaMemcpyDeviceToHost, st);
+        unsigned long long hs[3] = {0, 0, 0};
+        cudaMemcpyAsync(hs, stats, 24, cudaMemcpyDeviceToHost, st);
         ce = cudaStreamSynchronize(st);
         cudaFree(stats);
         if (tmp) cudaFree(tmp);
         if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_CUDA, "create: %s", cudaGetErrorString(ce)); }
         v->region_total_t0 = hs[0];
         v->region_max_t0 = hs[1];
+        v->V.max_pal = (uint32_t)(hs[2] < 0xffffffffull ? hs[2] : 0xffffffffull);
     }
     if (deferred) {  // the zero fill must land before uploads issued on other streams
         ce = cudaStreamSynchronize(st);
@@ -389,6 +393,8 @@ int csv_decode_volume_range(csv_volume* vol, int t, uint64_t brick_first, uint64
     P.eoff = vol->d_eoff;
     P.sres = vol->d_sres;
     P.entries = vol->d_entries;
+    P.wscratch = vol->d_wscratch;
+    P.wscratch_stride = kWScratchStride;
     CUDA_TRY(run_decode(vol->V, P, 0, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
                         vol->gws_ctas, vol->nsm, t, st, vol->timing ? vol->ev : nullptr));
     return CSV_OK;
@@ -420,6 +426,8 @@ int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, cons
     P.eoff = vol->d_eoff;
     P.sres = vol->d_sres;
     P.entries = vol->d_entries;
+    P.wscratch = vol->d_wscratch;
+    P.wscratch_stride = kWScratchStride;
     CUDA_TRY(run_decode(vol->V, P, 1, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
                         vol->gws_ctas, vol->nsm, 0, st, vol->timing ? vol->ev : nullptr));
     return CSV_OK;

@@ -20,6 +20,7 @@
 //                     raster (K3, decompress_volume) or Morton pool order (K4,
 //                     brick cache).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include "csv_device.cuh"
@@ -843,6 +844,7 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
 }
 
 #include "csv_replay_fast.cuh"
+#include "csv_replay_warp.cuh"
 
 // Coarsest-LOD raster (t == N): one voxel per brick.
 __global__ void k_root_raster(VolView V, Plan P) {
@@ -913,6 +915,37 @@ static void k2_launch_mode(int L, unsigned grid, size_t smem, const VolView& V, 
         default: k2_launch_one<MODE, 5>(grid, smem, V, P, st); break;
     }
 }
+// K2w: persistent warps (K2W_WARPS per CTA), as many CTAs as fit per SM
+template <int MODE, int L>
+static void k2w_launch_one(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
+    const size_t smem = (size_t)K2W_WARPS * wk::make_wlayout(L).bytes;
+    static int occ = 0;
+    if (!occ) {
+        cudaFuncSetAttribute(k2_warp<MODE, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_warp<MODE, L>, 32 * K2W_WARPS, smem);
+        if (occ < 1) occ = 1;
+    }
+    uint64_t want = (P.n + K2W_WARPS - 1) / K2W_WARPS;
+    uint64_t grid = (uint64_t)nsm * occ;
+    if (grid > want) grid = want;
+    k2_warp<MODE, L><<<(unsigned)grid, 32 * K2W_WARPS, smem, st>>>(V, P, counter);
+}
+template <int MODE>
+static void k2w_launch_mode(int L, const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
+    switch (L) {
+        case 1: k2w_launch_one<MODE, 1>(V, P, counter, nsm, st); break;
+        case 2: k2w_launch_one<MODE, 2>(V, P, counter, nsm, st); break;
+        case 3: k2w_launch_one<MODE, 3>(V, P, counter, nsm, st); break;
+        case 4: k2w_launch_one<MODE, 4>(V, P, counter, nsm, st); break;
+        default: k2w_launch_one<MODE, 5>(V, P, counter, nsm, st); break;
+    }
+}
+static bool k2w_disabled() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("CSVGPU_K2"); v = (e && strcmp(e, "cta") == 0) ? 1 : 0; }
+    return v == 1;
+}
+
 static void launch_k2_smem(int mode, int L, unsigned grid, size_t smem, const VolView& V, const Plan& P, cudaStream_t st) {
     if (mode == OUT_RASTER) k2_launch_mode<OUT_RASTER>(L, grid, smem, V, P, st);
     else k2_launch_mode<OUT_MORTON>(L, grid, smem, V, P, st);
@@ -927,7 +960,7 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
     k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
     cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
     if (e != cudaSuccess) return e;
-    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), st);   // K1 items, K2w bricks
     if (ev) cudaEventRecord(ev[1], st);
     if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
     else launch_k1<false>(V, P, counter, nsm, st);
@@ -936,9 +969,14 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
     int Ls = V.N - min_t;
     if (Ls > 5) Ls = 5;
     if (Ls < 1) Ls = 1;
-    size_t smem = k2_smem_bytes(Ls);
-    unsigned grid = (unsigned)(P.n < 0x7fffffffull ? P.n : 0x7fffffffull);
-    launch_k2_smem(mode, Ls, grid, smem, V, P, st);
+    if (V.max_pal <= 65535u && !k2w_disabled()) {   // u16 palette-index space
+        if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER>(Ls, V, P, counter + 1, nsm, st);
+        else k2w_launch_mode<OUT_MORTON>(Ls, V, P, counter + 1, nsm, st);
+    } else {
+        size_t smem = k2_smem_bytes(Ls);
+        unsigned grid = (unsigned)(P.n < 0x7fffffffull ? P.n : 0x7fffffffull);
+        launch_k2_smem(mode, Ls, grid, smem, V, P, st);
+    }
     if (V.N - min_t > 5 && gws) {
         unsigned g = (unsigned)(P.n < (uint64_t)gws_ctas ? P.n : (uint64_t)gws_ctas);
         if (V.N - min_t == 6) {

@@ -38,7 +38,10 @@ struct VolView {
     int64_t gx, gy, gz;        // brick grid
     uint64_t brick_begin;
     uint64_t nb;
+    uint32_t max_pal;          // longest palette (K2w works in u16 palette-index space)
 };
+
+constexpr uint32_t kWScratchStride = 4096;   // K2w scratch per warp slot (final-level parents, LMAX <= 5)
 
 // One decode call: n requests; request r decodes brick `brick[r]` at LOD lod[r].
 struct Plan {
@@ -56,6 +59,8 @@ struct Plan {
     uint8_t* entries;
     csv_result* res;           // [n] or nullptr
     unsigned long long* op_counts;   // K1 count mode (stats): 8 per-op totals, else nullptr
+    uint16_t* wscratch;        // K2w: per resident warp, palette base per final-level active parent
+    uint32_t wscratch_stride;  // u16 per warp slot
 };
 
 __device__ __forceinline__ uint64_t req_local(const VolView& V, const Plan& P, uint64_t r) {

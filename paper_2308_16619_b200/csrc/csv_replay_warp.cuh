@@ -1,0 +1,669 @@
+// csv_replay_warp.cuh -- K2w: one WARP per brick, persistent warps pulling
+// requests from a global counter.  Included by csv_decode.cu after the shared
+// K2 helpers (Raster, ekey, raster_of, op_eq, ...).
+//
+// Reference: _decode_kernel (codec.py:303-471) replays levels N..t+1, parents
+// in Morton order, 8 children each.  The GPU restatement keeps a brick inside
+// one warp (no CTA barriers, a dozen bricks in flight per SM) and works in
+// palette-index space (u16), so the coarse pyramid fits in ~9 KB of shared
+// memory per warp.  Per level:
+//
+//  * fill: every parent's 8 children get the parent's value (stop fill /
+//    occupancy skip, codec.py:367-370, :458-463); active parents (those the
+//    reference visits) are ranked by a popcount prefix of the level's mask,
+//    which is also the index of their 8 entries (K1's entry groups).
+//  * active pass: one lane per ACTIVE parent (compacted, so no lane idles on
+//    the 70 % of parents that are constant) evaluates its 8 children
+//    (codec.py:400-457); the palette base i_p is a warp scan of the P_a
+//    counts of the preceding parents in entry order.
+//  * chain rounds: an even-coordinate neighbour op reuses the already decoded
+//    child of the -1 neighbour parent (codec.py:422-423), whose local index is
+//    c | (1 << axis) -- one more odd coordinate.  Resolving children by
+//    decreasing popcount of the local index (7 | 3,5,6 | 1,2,4 | 0) therefore
+//    takes exactly three rounds and never a loop.
+//
+// Coarse levels keep their children in the shared level array.  The final
+// level is swept plane by plane (parent z): the children of the current
+// parent plane and the odd-z voxel plane below live in a 3-plane ring, the
+// inactive parents are written to HBM straight from the fill, the active ones
+// after their rounds.
+
+namespace wk {
+
+__host__ __device__ constexpr uint32_t wofs(int j) {   // u16 offset of level N-j (root j = 0), 8-aligned
+    return j == 0 ? 0u : 8u + ((1u << (3 * j)) - 8u) / 7u;
+}
+__host__ __device__ constexpr uint32_t al16(uint32_t v) { return (v + 15u) & ~15u; }
+__host__ __device__ constexpr uint32_t umax(uint32_t a, uint32_t b) { return a > b ? a : b; }
+
+struct WLayout {
+    uint32_t lev, pm, cm, wpre, ring, plist, pdesc, clist, cdesc, bytes;   // byte offsets in one warp's slice
+};
+__host__ __device__ constexpr WLayout make_wlayout(int L) {
+    WLayout Y{};
+    const uint32_t maxP = 1u << (3 * (L - 1));            // final-level parents (= coarse children max)
+    const uint32_t W = (maxP + 31) / 32;
+    const uint32_t R = 1u << (L - 1);
+    const uint32_t ringb = 3u * (2u * R) * (2u * R) * 2u;   // three voxel planes of (2R)^2 u16
+    const uint32_t cpar = L >= 2 ? (1u << (3 * (L - 2))) : 1u;   // coarse-level parents (max)
+    Y.lev = 0;
+    Y.pm = al16(wofs(L) * 2);
+    Y.cm = al16(Y.pm + 4 * W);
+    Y.wpre = al16(Y.cm + 4 * W);
+    Y.ring = al16(Y.wpre + 2 * W);
+    Y.plist = al16(Y.ring + ringb);                       // final: per-plane active list (u32) + pend (u16)
+    Y.pdesc = al16(Y.plist + 4 * R * R);
+    const uint32_t fin_end = al16(Y.pdesc + 2 * R * R);
+    Y.clist = Y.ring;                                     // coarse: active list (u16) + pend (u16), aliases the ring
+    Y.cdesc = al16(Y.clist + 2 * cpar);
+    const uint32_t coa_end = al16(Y.cdesc + 2 * cpar);
+    Y.bytes = umax(fin_end, coa_end);
+    return Y;
+}
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint64_t ONES = 0x0101010101010101ull;
+
+__device__ __forceinline__ void put_result(const Plan& P, uint64_t r, int st, int stream, int64_t pos, int64_t ci,
+                                           int64_t di) {
+    if (P.res) {
+        csv_result o;
+        o.status = st; o.stream = stream; o.pos = pos; o.ci = ci; o.di = di;
+        P.res[r] = o;
+    }
+}
+
+__device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
+__device__ __forceinline__ unsigned long long warp_min64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = umin64(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
+
+// Exclusive popcount prefix of mask words [0, W) into wpre; returns the total (warp-uniform).
+__device__ __forceinline__ uint32_t rank_prefix(const uint32_t* pm, uint32_t W, uint16_t* wpre, int lane) {
+    uint32_t run = 0;
+    for (uint32_t w0 = 0; w0 < W; w0 += 32) {
+        const uint32_t i = w0 + lane;
+        const uint32_t v = i < W ? __popc(pm[i]) : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (i < W) wpre[i] = (uint16_t)(run + inc - v);
+        run += __shfl_sync(FULL, inc, 31);
+    }
+    __syncwarp();
+    return run;
+}
+
+// SWAR byte masks (0x01 per child byte) over the 8 entries of a group
+__device__ __forceinline__ uint64_t m_op7(uint64_t w) { return w & (w >> 1) & (w >> 2) & ONES; }
+__device__ __forceinline__ uint64_t m_op5(uint64_t w) { return w & ~(w >> 1) & (w >> 2) & ONES; }
+__device__ __forceinline__ uint64_t m_pal(uint64_t w) { return (w >> 2) & ONES & ~m_op7(w); }   // ops 4, 5, 6
+__device__ __forceinline__ uint64_t m_op6(uint64_t w) { return ~w & (w >> 1) & (w >> 2) & ONES; }
+__device__ __forceinline__ uint32_t first_byte(uint64_t m) { return (uint32_t)(__ffsll((long long)m) - 1) >> 3; }
+__device__ __forceinline__ uint64_t valid_mask(uint32_t nvalid, uint32_t ent0) {
+    const uint32_t nv = nvalid > ent0 ? min(nvalid - ent0, 8u) : 0u;
+    return nv == 8 ? ~0ull : ((1ull << (8 * nv)) - 1ull);
+}
+
+// Inclusive warp scan (u32).
+__device__ __forceinline__ uint32_t warp_incl(uint32_t v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+// Values of the 8 children of one active parent (codec.py:400-425): R_p and
+// odd-coordinate neighbour ops resolved here, even-coordinate neighbour ops
+// marked pending (axis + 1, 2 bits per child), boundary violations flagged.
+// bf: bit 2a = parent at coordinate 0 on axis a, bit 2a+1 = at the maximum.
+struct Group {
+    uint32_t v[8];
+    uint32_t pend;   // 2 bits per child: 0 none, 1 x, 2 y, 3 z
+    uint32_t bn;     // BAD_NEIGHBOR children (bit c)
+};
+__device__ __forceinline__ void eval_group(uint64_t w, uint32_t pv, uint32_t pxp, uint32_t pyp, uint32_t pzp,
+                                           uint32_t bf, Group& g) {
+    const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+    g.pend = 0;
+    g.bn = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t op = ((c < 4 ? lo : hi) >> (8 * (c & 3))) & 7u;
+        const bool ox = c & 1, oy = c & 2, oz = c & 4;
+        uint32_t val = pv;
+        if (ox) val = op == 1u ? pxp : val;
+        if (oy) val = op == 2u ? pyp : val;
+        if (oz) val = op == 3u ? pzp : val;
+        g.v[c] = val;
+        // even coordinate at 0 or odd coordinate at the maximum: no neighbour (codec.py:416-417)
+        const uint32_t bx = (bf >> (ox ? 1 : 0)) & 1u, by = (bf >> (oy ? 3 : 2)) & 1u, bz = (bf >> (oz ? 5 : 4)) & 1u;
+        const bool bad = (op == 1u && bx) || (op == 2u && by) || (op == 3u && bz);
+        uint32_t pa = 0;
+        if (!ox && op == 1u) pa = 1u;
+        if (!oy && op == 2u) pa = 2u;
+        if (!oz && op == 3u) pa = 3u;
+        if (bad) { pa = 0; g.bn |= 1u << c; }
+        g.pend |= pa << (2 * c);
+    }
+}
+
+// Error key of one group (codec.py:396-457 order per entry: BAD_OP, LEAF_STOP, op-specific).
+__device__ __forceinline__ unsigned long long group_errkey(uint32_t ent0, uint64_t w, uint64_t vmask, bool leaf,
+                                                          uint32_t bn8) {
+    unsigned long long k = ~0ull;
+    const uint64_t bad = m_op7(w) & vmask;
+    if (bad) k = umin64(k, ekey(ent0 + first_byte(bad), 0, CSV_ST_BAD_OP));
+    if (leaf) {
+        const uint64_t ls = (w >> 3) & ONES & vmask & ~bad;
+        if (ls) k = umin64(k, ekey(ent0 + first_byte(ls), 1, CSV_ST_LEAF_STOP));
+    }
+    uint64_t bn = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) bn |= (uint64_t)((bn8 >> c) & 1u) << (8 * c);
+    bn &= vmask;
+    if (bn) k = umin64(k, ekey(ent0 + first_byte(bn), 2, CSV_ST_BAD_NEIGHBOR));
+    return k;
+}
+
+// Palette ops of a group (P_last / P_delta / P_advance, codec.py:426-457):
+// calls put(c, idx) for each; returns the first range-error key.
+template <typename Put>
+__device__ __forceinline__ unsigned long long palette_children(uint64_t w, uint64_t pmask, int32_t ipq, uint32_t plen,
+                                                              uint32_t ent0, uint64_t vmask, Put put) {
+    unsigned long long key = ~0ull;
+    const uint64_t m6 = m_op6(w);
+    while (pmask) {
+        const uint32_t c = first_byte(pmask);
+        pmask &= pmask - 1;
+        const uint32_t e = (uint32_t)(w >> (8 * c)) & 0xFFu, op = e & 7u;
+        const int32_t ip = ipq + (int32_t)prefix_bytes(m6, (int)c);
+        int32_t idx = op == 4u ? ip : (op == 5u ? ip - (int32_t)(e >> 4) - 1 : ip + 1);
+        const int st = idx < 0 ? CSV_ST_DELTA_RANGE : (idx >= (int32_t)plen ? CSV_ST_PALETTE_RANGE : 0);
+        if (st && ((vmask >> (8 * c)) & 1u)) key = umin64(key, ekey(ent0 + c, 2, st));
+        idx = min(max(idx, 0), (int32_t)plen - 1);
+        put(c, (uint32_t)idx);
+    }
+    return key;
+}
+
+struct Brick {
+    uint64_t r;
+    int N, t, n;
+    uint32_t plen;
+    const uint32_t* pal;
+    Raster R;
+    uint32_t pitch, plane;
+    uint32_t* out_m;
+    bool al8, al16;
+    const uint8_t* Ec;  uint32_t capc;   // coarse entries, entry capacity (bytes)
+    const uint8_t* Ed;  uint32_t capd;
+    uint16_t* ipb;                       // per-warp scratch: palette base per final-level active parent
+    csv_stream_result src, srd;
+};
+
+// Store the 8 children (palette labels) of final-level parent q = (px, py, pz).
+template <int MODE>
+__device__ __forceinline__ void store_children(const Brick& B, const Plan& P, uint32_t q, uint32_t px, uint32_t py,
+                                               uint32_t pz, const uint32_t (&lab)[8]) {
+    if (MODE == OUT_MORTON) {
+        uint32_t* g = B.out_m + 8ull * q;
+        if (B.al16) {
+            reinterpret_cast<uint4*>(g)[0] = make_uint4(lab[0], lab[1], lab[2], lab[3]);
+            reinterpret_cast<uint4*>(g)[1] = make_uint4(lab[4], lab[5], lab[6], lab[7]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) g[c] = lab[c];
+        }
+    } else if (B.al8) {
+        uint32_t* g = B.R.base + ((2 * pz) * B.plane + (2 * py) * B.pitch + 2 * px);
+        *reinterpret_cast<uint2*>(g) = make_uint2(lab[0], lab[1]);
+        *reinterpret_cast<uint2*>(g + B.pitch) = make_uint2(lab[2], lab[3]);
+        *reinterpret_cast<uint2*>(g + B.plane) = make_uint2(lab[4], lab[5]);
+        *reinterpret_cast<uint2*>(g + B.plane + B.pitch) = make_uint2(lab[6], lab[7]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            uint32_t* pp = raster_of(B.R, P, 8 * q + c);
+            if (pp) *pp = lab[c];
+        }
+    }
+}
+
+// Error epilogue (warp): status/stream/nibble position of the winning key.
+__device__ __noinline__ void report_error(const Plan& P, uint64_t r, const uint8_t* Eb, uint32_t ecap,
+                                          csv_stream_result sr, unsigned long long ek, bool leaf, int lane) {
+    const uint32_t ent = (uint32_t)(ek >> 8);
+    const int code = (int)(ek & 0xF);
+    int st;
+    int64_t pos;
+    if (code == EK_UNDERRUN_NV) {
+        if ((sr.flags & CSV_SF_PARTIAL) && leaf && (sr.partial_op & 8u)) {
+            st = CSV_ST_LEAF_STOP;
+            pos = (int64_t)sr.fail_nibble - 1;
+        } else {
+            st = CSV_ST_UNDERRUN;
+            pos = (sr.flags & CSV_SF_FAILED) ? (int64_t)sr.fail_nibble : (int64_t)ent;
+        }
+    } else {
+        uint32_t cnt = 0;      // nibble index of entry `ent` = ent + #payload nibbles before it
+        for (uint32_t g = lane; g < (ent + 7) / 8; g += 32) {
+            uint64_t w = (8 * g + 8 <= ecap) ? __ldg(reinterpret_cast<const uint64_t*>(Eb) + g) : 0ull;
+            uint32_t lim = ent - 8 * g;
+            uint64_t m = m_op5(w);
+            if (lim < 8) m &= (1ull << (8 * lim)) - 1ull;
+            cnt += __popcll(m);
+        }
+        pos = (int64_t)ent + (int64_t)warp_sum(cnt);
+        st = code;
+        if (code == CSV_ST_DELTA_RANGE) pos += 1;   // reported at the payload nibble
+    }
+    if (lane == 0) put_result(P, r, st, leaf ? 1 : 0, pos, 0, 0);
+}
+
+// -1 / +1 neighbour along an axis of Morton index j (the axis' bits selected by M)
+__device__ __forceinline__ uint32_t morton_dec(uint32_t j, uint32_t M) { return (((j & M) - 1u) & M) | (j & ~M); }
+__device__ __forceinline__ uint32_t morton_inc(uint32_t j, uint32_t M) { return ((((j & M) | ~M) + 1u) & M) | (j & ~M); }
+
+// ---------------------------------------------------------------- coarse level (Morton, smem)
+// Parents at level N - j (j bits per axis), children kept in the level array.
+// Returns the warp-uniform error key; adds the level's payload nibbles to pdl.
+__device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j, uint16_t* lev, const uint32_t* pm,
+                                                          uint32_t* cm, uint16_t* wpre, uint16_t* list,
+                                                          uint16_t* pdesc, uint32_t& cur_c, uint32_t& ip_run,
+                                                          uint32_t& pdl, int lane) {
+    const uint32_t Pn = 1u << (3 * j);
+    const uint32_t W = (Pn + 31) >> 5;
+    const uint16_t* plev = lev + wofs(j);
+    uint16_t* clev = lev + wofs(j + 1);
+    const uint32_t Mx = axis_mask(0, j), My = axis_mask(1, j), Mz = axis_mask(2, j);        // parent level
+    const uint32_t Cx = axis_mask(0, j + 1), Cy = axis_mask(1, j + 1), Cz = axis_mask(2, j + 1);   // child level
+    const uint32_t nact = rank_prefix(pm, W, wpre, lane);
+    const uint32_t e0 = cur_c, nvalid = B.src.n_entries;
+    unsigned long long ek = ~0ull;
+    if ((uint64_t)e0 + 8ull * nact > nvalid) ek = ekey(nvalid, 0, EK_UNDERRUN_NV);
+    const uint32_t CW = (8 * Pn + 31) >> 5;
+    for (uint32_t i = lane; i < CW; i += 32) cm[i] = 0u;
+    // fill: children repeat the parent (codec.py:458-463); active list by rank
+    for (uint32_t q0 = 0; q0 < Pn; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        if (q < Pn) {
+            const uint32_t pv = plev[q];
+            const uint32_t pp = pv | (pv << 16);
+            reinterpret_cast<uint4*>(clev + 8 * q)[0] = make_uint4(pp, pp, pp, pp);
+            const uint32_t mw = pm[q >> 5];
+            if ((mw >> (q & 31)) & 1u) list[wpre[q >> 5] + __popc(mw & ((1u << (q & 31)) - 1u))] = (uint16_t)q;
+        }
+    }
+    __syncwarp();
+    uint8_t* const cmb = reinterpret_cast<uint8_t*>(cm);
+    uint32_t anyp = 0;
+    for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const uint32_t ent0 = e0 + 8 * k;
+        const uint64_t w = (k < nact && ent0 + 8 <= B.capc) ? __ldg(reinterpret_cast<const uint64_t*>(B.Ec + ent0)) : 0ull;
+        // palette base: i_p advances (P_a) of the preceding parents, in entry order (codec.py:453-457)
+        const uint32_t c6 = __popcll(m_op6(w)), inc6 = warp_incl(c6, lane);
+        const int32_t ipq = (int32_t)(ip_run + inc6 - c6);
+        ip_run += __shfl_sync(FULL, inc6, 31);
+        if (k < nact) {
+            const uint32_t q = list[k];
+            const uint64_t vmask = valid_mask(nvalid, ent0);
+            pdl += __popcll(m_op5(w) & vmask);
+            const uint32_t pv = plev[q];
+            const uint32_t qx = q & Mx, qy = q & My, qz = q & Mz;
+            const uint32_t bf = (qx == 0) | ((qx == Mx) << 1) | ((qy == 0) << 2) | ((qy == My) << 3) |
+                                ((qz == 0) << 4) | ((qz == Mz) << 5);
+            const uint32_t pxp = qx != Mx ? plev[morton_inc(q, Mx)] : 0u;
+            const uint32_t pyp = qy != My ? plev[morton_inc(q, My)] : 0u;
+            const uint32_t pzp = qz != Mz ? plev[morton_inc(q, Mz)] : 0u;
+            Group g;
+            eval_group(w, pv, pxp, pyp, pzp, bf, g);
+            reinterpret_cast<uint4*>(clev + 8 * q)[0] =
+                make_uint4(g.v[0] | (g.v[1] << 16), g.v[2] | (g.v[3] << 16), g.v[4] | (g.v[5] << 16), g.v[6] | (g.v[7] << 16));
+            cmb[q] = (uint8_t)(((~(w >> 3) & ONES) * 0x0102040810204080ull) >> 56);   // no stop: visited next level
+            pdesc[k] = (uint16_t)g.pend;
+            anyp |= g.pend;
+            const uint64_t pmk = m_pal(w);
+            unsigned long long pk = ~0ull;
+            if (pmk) {
+                pk = palette_children(w, pmk, ipq, B.plen, ent0, vmask,
+                                      [&](uint32_t c, uint32_t idx) { clev[8 * q + c] = (uint16_t)idx; });
+            }
+            if (((m_op7(w) & vmask) != 0) | (g.bn != 0) | (pk != ~0ull))
+                ek = umin64(ek, umin64(pk, group_errkey(ent0, w, vmask, false, g.bn)));
+        }
+    }
+    __syncwarp();
+    if (__any_sync(FULL, anyp != 0u)) {
+        // rounds by decreasing popcount of the child index: targets are final
+#pragma unroll
+        for (int rd = 1; rd <= 3; ++rd) {
+            for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                const uint32_t pd = k < nact ? pdesc[k] : 0u;
+                if (pd) {
+                    const uint32_t q = list[k];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        if (__popc(c) != 3 - rd) continue;
+                        const uint32_t a1 = (pd >> (2 * c)) & 3u;
+                        if (!a1) continue;
+                        const uint32_t M = a1 == 1 ? Cx : (a1 == 2 ? Cy : Cz);
+                        const uint32_t jj = (q << 3) | c;
+                        clev[jj] = clev[morton_dec(jj, M)];
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    cur_c = e0 + 8 * nact;
+    return warp_min64(ek);
+}
+
+// ---------------------------------------------------------------- final level (plane sweep)
+// Ring voxel plane z (u16, (2R)^2) at ring + (z % 3) * (2R)^2; child (cx, cy) at cy * 2R + cx.
+template <int MODE, int RR>
+__device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const Plan& P, const uint16_t* plev,
+                                                         const uint32_t* pm, uint16_t* wpre, uint16_t* ring,
+                                                         uint32_t* plist, uint16_t* pdesc, uint32_t& cur,
+                                                         uint32_t& ip_run, uint32_t& pdl, int lane) {
+    constexpr uint32_t Pn = RR * RR * RR, W = (Pn + 31) / 32;
+    constexpr uint32_t PP = RR * RR;                    // parents per plane
+    constexpr uint32_t S2 = 2 * RR;                     // children per row
+    constexpr uint32_t PL = S2 * S2;                    // u16 per voxel plane
+    const bool leaf = B.t == 0;
+    const uint32_t nact = rank_prefix(pm, W, wpre, lane);
+    const uint8_t* const E = leaf ? B.Ed : B.Ec;
+    const uint32_t cap = leaf ? B.capd : B.capc;
+    const uint32_t nvalid = leaf ? B.srd.n_entries : B.src.n_entries;
+    const uint32_t e0 = cur;
+    unsigned long long ek = ~0ull;
+    if ((uint64_t)e0 + 8ull * nact > nvalid) ek = ekey(nvalid, 0, EK_UNDERRUN_NV);
+    // palette base per active parent, in entry (rank) order (codec.py:453-457) -> per-warp scratch
+    for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const uint32_t ent0 = e0 + 8 * k;
+        const uint64_t w = (k < nact && ent0 + 8 <= cap) ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+        const uint32_t c6 = __popcll(m_op6(w)), inc6 = warp_incl(c6, lane);
+        if (k < nact) B.ipb[k] = (uint16_t)(ip_run + inc6 - c6);
+        ip_run += __shfl_sync(FULL, inc6, 31);
+    }
+    __syncwarp();
+    uint32_t* const ring32 = reinterpret_cast<uint32_t*>(ring);
+    for (uint32_t pz = 0; pz < RR; ++pz) {
+        const uint32_t sz = spread3_u32(pz) << 2;
+        uint32_t* const r0 = ring32 + ((2 * pz) % 3) * (PL / 2);       // voxel plane 2pz   (u32 = 2 children in x)
+        uint32_t* const r1 = ring32 + ((2 * pz + 1) % 3) * (PL / 2);   // voxel plane 2pz+1
+        // ---- fill: ring <- parent values; inactive parents straight to HBM; active list
+        uint32_t nl = 0;
+        for (uint32_t i0 = 0; i0 < PP; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool ok = i < PP;
+            const uint32_t px = i % RR, py = i / RR;
+            const uint32_t q = spread3_u32(px) | (spread3_u32(py) << 1) | sz;
+            uint32_t mw = 0, pv = 0;
+            if (ok) {
+                pv = plev[q];
+                mw = pm[q >> 5];
+                const uint32_t pp = pv | (pv << 16);
+                r0[(2 * py) * RR + px] = pp;
+                r0[(2 * py + 1) * RR + px] = pp;
+                r1[(2 * py) * RR + px] = pp;
+                r1[(2 * py + 1) * RR + px] = pp;
+            }
+            const bool act = ok && ((mw >> (q & 31)) & 1u);
+            const uint32_t bal = __ballot_sync(FULL, act);
+            if (act) {
+                plist[nl + __popc(bal & lanemask_lt(lane))] =
+                    i | ((wpre[q >> 5] + __popc(mw & ((1u << (q & 31)) - 1u))) << 16);
+            } else if (ok) {
+                const uint32_t l = __ldg(B.pal + pv);
+                const uint32_t lab[8] = {l, l, l, l, l, l, l, l};
+                store_children<MODE>(B, P, q, px, py, pz, lab);
+            }
+            nl += __popc(bal);
+        }
+        __syncwarp();
+        // ---- active parents of this plane: one lane each
+        uint32_t anyp = 0;
+        for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            if (k < nl) {
+                const uint32_t it = plist[k];
+                const uint32_t i = it & 0xFFFFu, rank = it >> 16;
+                const uint32_t px = i % RR, py = i / RR;
+                const uint32_t sx = spread3_u32(px), sy = spread3_u32(py) << 1;
+                const uint32_t q = sx | sy | sz;
+                const uint32_t ent0 = e0 + 8 * rank;
+                const uint64_t w = ent0 + 8 <= cap ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+                const uint64_t vmask = valid_mask(nvalid, ent0);
+                pdl += __popcll(m_op5(w) & vmask);
+                const uint32_t pv = plev[q];
+                const uint32_t bf = (px == 0) | ((px == RR - 1) << 1) | ((py == 0) << 2) | ((py == RR - 1) << 3) |
+                                    ((pz == 0) << 4) | ((pz == RR - 1) << 5);
+                const uint32_t pxp = px + 1 < RR ? plev[spread3_u32(px + 1) | sy | sz] : 0u;
+                const uint32_t pyp = py + 1 < RR ? plev[sx | (spread3_u32(py + 1) << 1) | sz] : 0u;
+                const uint32_t pzp = pz + 1 < RR ? plev[sx | sy | (spread3_u32(pz + 1) << 2)] : 0u;
+                Group g;
+                eval_group(w, pv, pxp, pyp, pzp, bf, g);
+                r0[(2 * py) * RR + px] = g.v[0] | (g.v[1] << 16);
+                r0[(2 * py + 1) * RR + px] = g.v[2] | (g.v[3] << 16);
+                r1[(2 * py) * RR + px] = g.v[4] | (g.v[5] << 16);
+                r1[(2 * py + 1) * RR + px] = g.v[6] | (g.v[7] << 16);
+                pdesc[k] = (uint16_t)g.pend;
+                anyp |= g.pend;
+                const uint64_t pmk = m_pal(w);
+                unsigned long long pk = ~0ull;
+                if (pmk) {
+                    const int32_t ipq = B.ipb[rank];
+                    uint16_t* const p0 = reinterpret_cast<uint16_t*>(r0);
+                    uint16_t* const p1 = reinterpret_cast<uint16_t*>(r1);
+                    pk = palette_children(w, pmk, ipq, B.plen, ent0, vmask, [&](uint32_t c, uint32_t idx) {
+                        uint16_t* pl = (c & 4) ? p1 : p0;
+                        pl[(2 * py + ((c >> 1) & 1)) * S2 + 2 * px + (c & 1)] = (uint16_t)idx;
+                    });
+                }
+                const uint64_t errs = m_op7(w) | (leaf ? (w >> 3) & ONES : 0ull);
+                if (((errs & vmask) != 0) | (g.bn != 0) | (pk != ~0ull))
+                    ek = umin64(ek, umin64(pk, group_errkey(ent0, w, vmask, leaf, g.bn)));
+            }
+        }
+        __syncwarp();
+        const uint16_t* const pr = ring + ((2 * pz + 2) % 3) * PL;   // voxel plane 2pz-1
+        uint16_t* const p0 = ring + ((2 * pz) % 3) * PL;
+        uint16_t* const p1 = ring + ((2 * pz + 1) % 3) * PL;
+        // ---- chain rounds: child c <- child c | (1 << axis) of the -1 neighbour (ring)
+        if (__any_sync(FULL, anyp != 0u)) {
+#pragma unroll
+            for (int rd = 1; rd <= 3; ++rd) {
+                for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
+                    const uint32_t k = k0 + lane;
+                    const uint32_t pd = k < nl ? pdesc[k] : 0u;
+                    if (pd) {
+                        const uint32_t i = plist[k] & 0xFFFFu;
+                        const uint32_t cx0 = 2 * (i % RR), cy0 = 2 * (i / RR);
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            if (__popc(c) != 3 - rd) continue;
+                            const uint32_t a1 = (pd >> (2 * c)) & 3u;
+                            if (!a1) continue;
+                            const uint32_t cx = cx0 + (c & 1), cy = cy0 + ((c >> 1) & 1);
+                            uint16_t* const dst = ((c & 4) ? p1 : p0) + cy * S2 + cx;
+                            uint16_t val;
+                            if (a1 == 1u) val = dst[-1];
+                            else if (a1 == 2u) val = dst[-(int)S2];
+                            else val = ((c & 4) ? p0 : pr)[cy * S2 + cx];   // z - 1
+                            *dst = val;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        // ---- active parents to HBM
+        for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            if (k < nl) {
+                const uint32_t i = plist[k] & 0xFFFFu;
+                const uint32_t px = i % RR, py = i / RR;
+                const uint32_t q = spread3_u32(px) | (spread3_u32(py) << 1) | sz;
+                const uint32_t* const q0 = reinterpret_cast<const uint32_t*>(p0);
+                const uint32_t* const q1 = reinterpret_cast<const uint32_t*>(p1);
+                const uint32_t a = q0[(2 * py) * RR + px], b = q0[(2 * py + 1) * RR + px];
+                const uint32_t c = q1[(2 * py) * RR + px], d = q1[(2 * py + 1) * RR + px];
+                const uint32_t vv[8] = {a & 0xFFFFu, a >> 16, b & 0xFFFFu, b >> 16, c & 0xFFFFu, c >> 16, d & 0xFFFFu, d >> 16};
+                uint32_t lab[8];
+                const uint32_t l0 = __ldg(B.pal + vv[0]);
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) lab[cc] = vv[cc] == vv[0] ? l0 : __ldg(B.pal + vv[cc]);
+                store_children<MODE>(B, P, q, px, py, pz, lab);
+            }
+        }
+        __syncwarp();
+    }
+    cur = e0 + 8 * nact;
+    return warp_min64(ek);
+}
+
+}  // namespace wk
+
+#ifndef K2W_WPB
+#define K2W_WPB 2
+#endif
+constexpr int K2W_WARPS = K2W_WPB;
+
+template <int MODE, int LMAX>
+__global__ void __launch_bounds__(32 * K2W_WARPS) k2_warp(VolView V, Plan P, unsigned long long* counter) {
+    using namespace wk;
+    constexpr WLayout Y = make_wlayout(LMAX);
+    extern __shared__ __align__(16) uint8_t wsm[];
+    uint8_t* const base = wsm + (threadIdx.x >> 5) * Y.bytes;
+    uint16_t* const lev = reinterpret_cast<uint16_t*>(base + Y.lev);
+    uint32_t* const mA = reinterpret_cast<uint32_t*>(base + Y.pm);
+    uint32_t* const mB = reinterpret_cast<uint32_t*>(base + Y.cm);
+    uint16_t* const wpre = reinterpret_cast<uint16_t*>(base + Y.wpre);
+    uint16_t* const ring = reinterpret_cast<uint16_t*>(base + Y.ring);
+    uint32_t* const plist = reinterpret_cast<uint32_t*>(base + Y.plist);
+    uint16_t* const pdesc = reinterpret_cast<uint16_t*>(base + Y.pdesc);
+    uint16_t* const clist = reinterpret_cast<uint16_t*>(base + Y.clist);
+    uint16_t* const cdesc = reinterpret_cast<uint16_t*>(base + Y.cdesc);
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        __syncwarp();
+        unsigned long long rr = 0;
+        if (lane == 0) rr = atomicAdd(counter, 1ull);
+        rr = __shfl_sync(FULL, rr, 0);
+        if (rr >= P.n) break;
+        Brick B{};
+        B.r = rr;
+        const uint64_t b = req_local(V, P, rr);
+        B.t = req_lod(P, rr);
+        B.N = V.N;
+        if (b >= V.nb || B.t > B.N) { if (lane == 0) put_result(P, rr, -1, 0, 0, 0, 0); continue; }
+        B.n = B.N - B.t;
+        if (B.t < B.N && B.n > LMAX) continue;          // served by the global-workspace kernel
+        B.out_m = MODE == OUT_MORTON ? P.out + P.dst[rr] : nullptr;
+        B.plen = V.pal_len[b];
+        B.pal = V.palette + V.pal_off[b];
+        if (MODE == OUT_RASTER) {
+            const uint64_t gb = V.brick_begin + b;
+            const int64_t side = 1ll << B.n;
+            B.R.ox = (int64_t)(gb % V.gx) * side;
+            B.R.oy = (int64_t)((gb / V.gx) % V.gy) * side;
+            B.R.oz = (int64_t)(gb / (V.gx * V.gy)) * side;
+            B.R.base = P.out + ((B.R.oz - P.z_begin) * P.cy + B.R.oy) * P.cx + B.R.ox;
+            B.R.fast = B.R.ox + side <= P.cx && B.R.oy + side <= P.cy && B.R.oz >= P.z_begin &&
+                       B.R.oz + side <= P.z_end && (uint64_t)P.cx * P.cy * side < (1ull << 32);
+            B.pitch = (uint32_t)P.cx;
+            B.plane = (uint32_t)(P.cx * P.cy);
+            B.al8 = B.R.fast && (B.pitch & 1u) == 0u && (reinterpret_cast<uintptr_t>(B.R.base) & 7u) == 0u;
+        } else {
+            B.al16 = (reinterpret_cast<uintptr_t>(B.out_m) & 15u) == 0u;
+        }
+        if (B.plen == 0) { if (lane == 0) put_result(P, rr, CSV_ST_EMPTY_PALETTE, 0, 0, 0, 0); continue; }
+        if (B.t == B.N) {   // coarsest LOD: palette[0] (codec.py:514-516, container.py:178-182)
+            if (lane == 0) {
+                uint32_t* p = MODE == OUT_MORTON ? B.out_m : raster_of(B.R, P, 0);
+                if (p) *p = __ldg(B.pal);
+                put_result(P, rr, 0, 0, 0, 0, 0);
+            }
+            continue;
+        }
+        const uint32_t nc_raw = V.c_nib[b], nd_raw = B.t == 0 ? V.d_nib[b] : 0;
+        const uint32_t nc = eff_nibbles(V, b, 0), nd = B.t == 0 ? eff_nibbles(V, b, 1) : 0;
+        if (V.entropy) {   // state-word checks come first (codec.py:331-351)
+            if (nc_raw > 0 && V.c_bytes[b] < 4) { if (lane == 0) put_result(P, rr, CSV_ST_UNDERRUN, 0, 0, 0, 0); continue; }
+            if (B.t == 0 && nd_raw > 0 && V.d_bytes[b] < 4) { if (lane == 0) put_result(P, rr, CSV_ST_UNDERRUN, 1, 0, 0, 0); continue; }
+        }
+        B.src = P.sres[2 * rr];
+        B.srd = P.sres[2 * rr + 1];
+        const uint64_t eo0 = P.eoff[2 * rr], eo1 = P.eoff[2 * rr + 1], eo2 = P.eoff[2 * rr + 2];
+        if (lane == 0 && eo2 > eo0) {   // stage this brick's entries + gip in L2 ahead of the levels
+            const uint64_t lo = eo0 & ~15ull, hi = (eo2 + 15) & ~15ull;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(P.entries + lo), "r"((uint32_t)(hi - lo)) : "memory");
+        }
+        const uint32_t limc = stream_limit(V, b, B.t, 0), limd = B.t == 0 ? stream_limit(V, b, 0, 1) : 0u;
+        B.Ec = P.entries + eo0;
+        B.capc = (uint32_t)round32(limc);
+        B.Ed = P.entries + eo1;
+        B.capd = (uint32_t)round32(limd);
+        B.ipb = P.wscratch + (uint64_t)(blockIdx.x * K2W_WARPS + (threadIdx.x >> 5)) * P.wscratch_stride;
+        const bool trivial = (uint64_t)nc + nd == 0;     // relevant == 0: fill palette[0] (codec.py:353-358)
+        if (lane == 0) {
+            lev[0] = 0;
+            mA[0] = trivial ? 0u : 1u;
+        }
+        __syncwarp();
+        uint32_t cur_c = 0, cur_d = 0, pdc = 0, pdd = 0, ip_run = 0;
+        uint32_t* pm = mA;
+        uint32_t* cm = mB;
+        bool failed = false;
+        for (int j = 0; j + 1 < B.n; ++j) {      // parents at level N - j, children above the final level
+            const unsigned long long ek = coarse_level(B, j, lev, pm, cm, wpre, clist, cdesc, cur_c, ip_run, pdc, lane);
+            if (ek != ~0ull) { report_error(P, rr, B.Ec, B.capc, B.src, ek, false, lane); failed = true; break; }
+            uint32_t* tmp = pm; pm = cm; cm = tmp;
+        }
+        if (failed) continue;
+        const uint16_t* plev = lev + wofs(B.n - 1);
+        uint32_t& cur = B.t == 0 ? cur_d : cur_c;
+        uint32_t& pdl = B.t == 0 ? pdd : pdc;
+        unsigned long long ek;
+        switch (B.n) {
+            case 1: ek = final_sweep<MODE, 1>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
+            case 2: ek = final_sweep<MODE, 2>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
+            case 3: ek = final_sweep<MODE, 4>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
+            case 4: ek = final_sweep<MODE, (LMAX >= 4 ? 8 : 1)>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
+            default: ek = final_sweep<MODE, (LMAX >= 5 ? 16 : 1)>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
+        }
+        if (ek != ~0ull) {
+            if (B.t == 0) report_error(P, rr, B.Ed, B.capd, B.srd, ek, true, lane);
+            else report_error(P, rr, B.Ec, B.capc, B.src, ek, false, lane);
+            continue;
+        }
+        const int64_t ci = (int64_t)cur_c + warp_sum(pdc), di = (int64_t)cur_d + warp_sum(pdd);
+        if (lane == 0) {
+            int st = 0, stream = 0;
+            int64_t pos = 0;
+            if (V.entropy) {   // full consumption must land on the initial state (codec.py:464-470)
+                if (nc_raw > 0 && ci == (int64_t)nc_raw && (B.src.flags & CSV_SF_DESYNC)) { st = CSV_ST_DESYNC; stream = 0; pos = ci; }
+                else if (B.t == 0 && nd_raw > 0 && di == (int64_t)nd_raw && (B.srd.flags & CSV_SF_DESYNC)) { st = CSV_ST_DESYNC; stream = 1; pos = di; }
+            }
+            put_result(P, rr, st, stream, pos, ci, di);
+        }
+    }
+}
