@@ -916,28 +916,29 @@ static void k2_launch_mode(int L, unsigned grid, size_t smem, const VolView& V, 
     }
 }
 // K2w: persistent warps (K2W_WARPS per CTA), as many CTAs as fit per SM
-template <int MODE, int L>
+template <int MODE, int L, typename IT>
 static void k2w_launch_one(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
-    const size_t smem = (size_t)K2W_WARPS * wk::make_wlayout(L).bytes;
+    const size_t smem = (size_t)K2W_WARPS * wk::make_wlayout(L, sizeof(IT)).bytes;
     static int occ = 0;
     if (!occ) {
-        cudaFuncSetAttribute(k2_warp<MODE, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_warp<MODE, L>, 32 * K2W_WARPS, smem);
+        cudaFuncSetAttribute(k2_warp<MODE, L, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_warp<MODE, L, IT>, 32 * K2W_WARPS, smem);
         if (occ < 1) occ = 1;
+        if (occ * K2W_WARPS > 64) occ = 64 / K2W_WARPS;   // wscratch holds 64 warp slots per SM
     }
     uint64_t want = (P.n + K2W_WARPS - 1) / K2W_WARPS;
     uint64_t grid = (uint64_t)nsm * occ;
     if (grid > want) grid = want;
-    k2_warp<MODE, L><<<(unsigned)grid, 32 * K2W_WARPS, smem, st>>>(V, P, counter);
+    k2_warp<MODE, L, IT><<<(unsigned)grid, 32 * K2W_WARPS, smem, st>>>(V, P, counter);
 }
-template <int MODE>
+template <int MODE, typename IT>
 static void k2w_launch_mode(int L, const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
     switch (L) {
-        case 1: k2w_launch_one<MODE, 1>(V, P, counter, nsm, st); break;
-        case 2: k2w_launch_one<MODE, 2>(V, P, counter, nsm, st); break;
-        case 3: k2w_launch_one<MODE, 3>(V, P, counter, nsm, st); break;
-        case 4: k2w_launch_one<MODE, 4>(V, P, counter, nsm, st); break;
-        default: k2w_launch_one<MODE, 5>(V, P, counter, nsm, st); break;
+        case 1: k2w_launch_one<MODE, 1, IT>(V, P, counter, nsm, st); break;
+        case 2: k2w_launch_one<MODE, 2, IT>(V, P, counter, nsm, st); break;
+        case 3: k2w_launch_one<MODE, 3, IT>(V, P, counter, nsm, st); break;
+        case 4: k2w_launch_one<MODE, 4, IT>(V, P, counter, nsm, st); break;
+        default: k2w_launch_one<MODE, 5, IT>(V, P, counter, nsm, st); break;
     }
 }
 static bool k2w_disabled() {
@@ -960,7 +961,7 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
     k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
     cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
     if (e != cudaSuccess) return e;
-    cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), st);   // K1 items, K2w bricks
+    cudaMemsetAsync(counter, 0, 3 * sizeof(unsigned long long), st);   // K1 items, K2w u8 / u16 bricks
     if (ev) cudaEventRecord(ev[1], st);
     if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
     else launch_k1<false>(V, P, counter, nsm, st);
@@ -969,9 +970,13 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
     int Ls = V.N - min_t;
     if (Ls > 5) Ls = 5;
     if (Ls < 1) Ls = 1;
-    if (V.max_pal <= 65535u && !k2w_disabled()) {   // u16 palette-index space
-        if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER>(Ls, V, P, counter + 1, nsm, st);
-        else k2w_launch_mode<OUT_MORTON>(Ls, V, P, counter + 1, nsm, st);
+    if (V.max_pal <= 65535u && !k2w_disabled()) {   // palette-index space: u8 pass, then u16 for long palettes
+        if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint8_t>(Ls, V, P, counter + 1, nsm, st);
+        else k2w_launch_mode<OUT_MORTON, uint8_t>(Ls, V, P, counter + 1, nsm, st);
+        if (V.max_pal > 256u) {
+            if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint16_t>(Ls, V, P, counter + 2, nsm, st);
+            else k2w_launch_mode<OUT_MORTON, uint16_t>(Ls, V, P, counter + 2, nsm, st);
+        }
     } else {
         size_t smem = k2_smem_bytes(Ls);
         unsigned grid = (unsigned)(P.n < 0x7fffffffull ? P.n : 0x7fffffffull);

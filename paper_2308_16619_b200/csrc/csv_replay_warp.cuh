@@ -4,9 +4,10 @@
 //
 // Reference: _decode_kernel (codec.py:303-471) replays levels N..t+1, parents
 // in Morton order, 8 children each.  The GPU restatement keeps a brick inside
-// one warp (no CTA barriers, a dozen bricks in flight per SM) and works in
-// palette-index space (u16), so the coarse pyramid fits in ~9 KB of shared
-// memory per warp.  Per level:
+// one warp (no CTA barriers, a dozen or more bricks in flight per SM) and
+// works in palette-index space (u8 when the palette has <= 256 entries, else
+// u16 in a second pass), so a warp's whole working set is 9 KB (17 KB) of
+// shared memory.  Per level:
 //
 //  * fill: every parent's 8 children get the parent's value (stop fill /
 //    occupancy skip, codec.py:367-370, :458-463); active parents (those the
@@ -36,29 +37,79 @@ __host__ __device__ constexpr uint32_t wofs(int j) {   // u16 offset of level N-
 __host__ __device__ constexpr uint32_t al16(uint32_t v) { return (v + 15u) & ~15u; }
 __host__ __device__ constexpr uint32_t umax(uint32_t a, uint32_t b) { return a > b ? a : b; }
 
+// Per-warp shared-memory slice for LMAX = N - t levels, values of `isz` bytes
+// (u8 palette indices when the palette has <= 256 entries, else u16):
+//   lev   : level values t+1..N, root first (wofs)
+//   pm/cm : active-parent bitmask of the level / of its children
+//   wpre  : popcount prefix of pm per word (rank of an active parent)
+//   ring  : final level: voxel planes 2pz-1, 2pz, 2pz+1 (3 x (2R)^2 values)
+//   plist : final level: per-plane active parents (u8 index in the plane)
+//   pdesc : final level: their pending-chain descriptors (u16); aliases cm
+//   clist/cdesc : coarse levels: active list / descriptors (u16); alias the ring
 struct WLayout {
     uint32_t lev, pm, cm, wpre, ring, plist, pdesc, clist, cdesc, bytes;   // byte offsets in one warp's slice
 };
-__host__ __device__ constexpr WLayout make_wlayout(int L) {
+__host__ __device__ constexpr WLayout make_wlayout(int L, uint32_t isz) {
     WLayout Y{};
     const uint32_t maxP = 1u << (3 * (L - 1));            // final-level parents (= coarse children max)
     const uint32_t W = (maxP + 31) / 32;
     const uint32_t R = 1u << (L - 1);
-    const uint32_t ringb = 3u * (2u * R) * (2u * R) * 2u;   // three voxel planes of (2R)^2 u16
+    const uint32_t ringb = 3u * (2u * R) * (2u * R) * isz;
     const uint32_t cpar = L >= 2 ? (1u << (3 * (L - 2))) : 1u;   // coarse-level parents (max)
     Y.lev = 0;
-    Y.pm = al16(wofs(L) * 2);
+    Y.pm = al16(wofs(L) * isz);
     Y.cm = al16(Y.pm + 4 * W);
     Y.wpre = al16(Y.cm + 4 * W);
     Y.ring = al16(Y.wpre + 2 * W);
-    Y.plist = al16(Y.ring + ringb);                       // final: per-plane active list (u32) + pend (u16)
-    Y.pdesc = al16(Y.plist + 4 * R * R);
-    const uint32_t fin_end = al16(Y.pdesc + 2 * R * R);
-    Y.clist = Y.ring;                                     // coarse: active list (u16) + pend (u16), aliases the ring
-    Y.cdesc = al16(Y.clist + 2 * cpar);
-    const uint32_t coa_end = al16(Y.cdesc + 2 * cpar);
-    Y.bytes = umax(fin_end, coa_end);
+    Y.plist = al16(Y.ring + ringb);
+    uint32_t end = al16(Y.plist + R * R);
+    if (2 * R * R <= 4 * W) {
+        Y.pdesc = Y.cm;                                   // cm is dead during the final sweep
+    } else {
+        Y.pdesc = end;
+        end = al16(end + 2 * R * R);
+    }
+    if (4 * cpar <= ringb) {
+        Y.clist = Y.ring;
+    } else {
+        Y.clist = end;
+        end = al16(end + 4 * cpar);
+    }
+    Y.cdesc = Y.clist + 2 * cpar;
+    Y.bytes = end;
     return Y;
+}
+
+// value storage: u8 or u16 palette indices; P2 holds two x-adjacent children
+template <typename IT> struct IX;
+template <> struct IX<uint8_t> { using P2 = uint16_t; static constexpr uint32_t B = 8; };
+template <> struct IX<uint16_t> { using P2 = uint32_t; static constexpr uint32_t B = 16; };
+template <typename IT>
+__device__ __forceinline__ typename IX<IT>::P2 pack2(uint32_t a, uint32_t b) { return (typename IX<IT>::P2)(a | (b << IX<IT>::B)); }
+template <typename IT>
+__device__ __forceinline__ uint32_t lo2(uint32_t p) { return p & ((1u << IX<IT>::B) - 1u); }
+template <typename IT>
+__device__ __forceinline__ uint32_t hi2(uint32_t p) { return p >> IX<IT>::B; }
+// the 8 children of one parent, contiguous (Morton order), 8 or 16 bytes
+template <typename IT>
+__device__ __forceinline__ void store8(IT* p, const uint32_t (&v)[8]) {
+    if (sizeof(IT) == 1) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24),
+                                                  v[4] | (v[5] << 8) | (v[6] << 16) | (v[7] << 24));
+    } else {
+        *reinterpret_cast<uint4*>(p) = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16),
+                                                  v[6] | (v[7] << 16));
+    }
+}
+template <typename IT>
+__device__ __forceinline__ void store8_same(IT* p, uint32_t v) {
+    if (sizeof(IT) == 1) {
+        const uint32_t x = v * 0x01010101u;
+        *reinterpret_cast<uint2*>(p) = make_uint2(x, x);
+    } else {
+        const uint32_t x = v | (v << 16);
+        *reinterpret_cast<uint4*>(p) = make_uint4(x, x, x, x);
+    }
 }
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -281,14 +332,15 @@ __device__ __forceinline__ uint32_t morton_inc(uint32_t j, uint32_t M) { return 
 // ---------------------------------------------------------------- coarse level (Morton, smem)
 // Parents at level N - j (j bits per axis), children kept in the level array.
 // Returns the warp-uniform error key; adds the level's payload nibbles to pdl.
-__device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j, uint16_t* lev, const uint32_t* pm,
+template <typename IT>
+__device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j, IT* lev, const uint32_t* pm,
                                                           uint32_t* cm, uint16_t* wpre, uint16_t* list,
                                                           uint16_t* pdesc, uint32_t& cur_c, uint32_t& ip_run,
                                                           uint32_t& pdl, int lane) {
     const uint32_t Pn = 1u << (3 * j);
     const uint32_t W = (Pn + 31) >> 5;
-    const uint16_t* plev = lev + wofs(j);
-    uint16_t* clev = lev + wofs(j + 1);
+    const IT* plev = lev + wofs(j);
+    IT* clev = lev + wofs(j + 1);
     const uint32_t Mx = axis_mask(0, j), My = axis_mask(1, j), Mz = axis_mask(2, j);        // parent level
     const uint32_t Cx = axis_mask(0, j + 1), Cy = axis_mask(1, j + 1), Cz = axis_mask(2, j + 1);   // child level
     const uint32_t nact = rank_prefix(pm, W, wpre, lane);
@@ -301,9 +353,7 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
     for (uint32_t q0 = 0; q0 < Pn; q0 += 32) {
         const uint32_t q = q0 + lane;
         if (q < Pn) {
-            const uint32_t pv = plev[q];
-            const uint32_t pp = pv | (pv << 16);
-            reinterpret_cast<uint4*>(clev + 8 * q)[0] = make_uint4(pp, pp, pp, pp);
+            store8_same<IT>(clev + 8 * q, plev[q]);
             const uint32_t mw = pm[q >> 5];
             if ((mw >> (q & 31)) & 1u) list[wpre[q >> 5] + __popc(mw & ((1u << (q & 31)) - 1u))] = (uint16_t)q;
         }
@@ -332,8 +382,7 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
             const uint32_t pzp = qz != Mz ? plev[morton_inc(q, Mz)] : 0u;
             Group g;
             eval_group(w, pv, pxp, pyp, pzp, bf, g);
-            reinterpret_cast<uint4*>(clev + 8 * q)[0] =
-                make_uint4(g.v[0] | (g.v[1] << 16), g.v[2] | (g.v[3] << 16), g.v[4] | (g.v[5] << 16), g.v[6] | (g.v[7] << 16));
+            store8<IT>(clev + 8 * q, g.v);
             cmb[q] = (uint8_t)(((~(w >> 3) & ONES) * 0x0102040810204080ull) >> 56);   // no stop: visited next level
             pdesc[k] = (uint16_t)g.pend;
             anyp |= g.pend;
@@ -341,7 +390,7 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
             unsigned long long pk = ~0ull;
             if (pmk) {
                 pk = palette_children(w, pmk, ipq, B.plen, ent0, vmask,
-                                      [&](uint32_t c, uint32_t idx) { clev[8 * q + c] = (uint16_t)idx; });
+                                      [&](uint32_t c, uint32_t idx) { clev[8 * q + c] = (IT)idx; });
             }
             if (((m_op7(w) & vmask) != 0) | (g.bn != 0) | (pk != ~0ull))
                 ek = umin64(ek, umin64(pk, group_errkey(ent0, w, vmask, false, g.bn)));
@@ -377,10 +426,10 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
 
 // ---------------------------------------------------------------- final level (plane sweep)
 // Ring voxel plane z (u16, (2R)^2) at ring + (z % 3) * (2R)^2; child (cx, cy) at cy * 2R + cx.
-template <int MODE, int RR>
-__device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const Plan& P, const uint16_t* plev,
-                                                         const uint32_t* pm, uint16_t* wpre, uint16_t* ring,
-                                                         uint32_t* plist, uint16_t* pdesc, uint32_t& cur,
+template <int MODE, int RR, typename IT>
+__device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const Plan& P, const IT* plev,
+                                                         const uint32_t* pm, uint16_t* wpre, IT* ring,
+                                                         uint8_t* plist, uint16_t* pdesc, uint32_t& cur,
                                                          uint32_t& ip_run, uint32_t& pdl, int lane) {
     constexpr uint32_t Pn = RR * RR * RR, W = (Pn + 31) / 32;
     constexpr uint32_t PP = RR * RR;                    // parents per plane
@@ -404,11 +453,12 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
         ip_run += __shfl_sync(FULL, inc6, 31);
     }
     __syncwarp();
-    uint32_t* const ring32 = reinterpret_cast<uint32_t*>(ring);
+    using P2 = typename IX<IT>::P2;
+    P2* const ring2 = reinterpret_cast<P2*>(ring);
     for (uint32_t pz = 0; pz < RR; ++pz) {
         const uint32_t sz = spread3_u32(pz) << 2;
-        uint32_t* const r0 = ring32 + ((2 * pz) % 3) * (PL / 2);       // voxel plane 2pz   (u32 = 2 children in x)
-        uint32_t* const r1 = ring32 + ((2 * pz + 1) % 3) * (PL / 2);   // voxel plane 2pz+1
+        P2* const r0 = ring2 + ((2 * pz) % 3) * (PL / 2);       // voxel plane 2pz   (2 children in x per P2)
+        P2* const r1 = ring2 + ((2 * pz + 1) % 3) * (PL / 2);   // voxel plane 2pz+1
         // ---- fill: ring <- parent values; inactive parents straight to HBM; active list
         uint32_t nl = 0;
         for (uint32_t i0 = 0; i0 < PP; i0 += 32) {
@@ -420,7 +470,7 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
             if (ok) {
                 pv = plev[q];
                 mw = pm[q >> 5];
-                const uint32_t pp = pv | (pv << 16);
+                const P2 pp = pack2<IT>(pv, pv);
                 r0[(2 * py) * RR + px] = pp;
                 r0[(2 * py + 1) * RR + px] = pp;
                 r1[(2 * py) * RR + px] = pp;
@@ -429,8 +479,7 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
             const bool act = ok && ((mw >> (q & 31)) & 1u);
             const uint32_t bal = __ballot_sync(FULL, act);
             if (act) {
-                plist[nl + __popc(bal & lanemask_lt(lane))] =
-                    i | ((wpre[q >> 5] + __popc(mw & ((1u << (q & 31)) - 1u))) << 16);
+                plist[nl + __popc(bal & lanemask_lt(lane))] = (uint8_t)i;
             } else if (ok) {
                 const uint32_t l = __ldg(B.pal + pv);
                 const uint32_t lab[8] = {l, l, l, l, l, l, l, l};
@@ -444,11 +493,11 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
         for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
             const uint32_t k = k0 + lane;
             if (k < nl) {
-                const uint32_t it = plist[k];
-                const uint32_t i = it & 0xFFFFu, rank = it >> 16;
+                const uint32_t i = plist[k];
                 const uint32_t px = i % RR, py = i / RR;
                 const uint32_t sx = spread3_u32(px), sy = spread3_u32(py) << 1;
                 const uint32_t q = sx | sy | sz;
+                const uint32_t rank = wpre[q >> 5] + __popc(pm[q >> 5] & ((1u << (q & 31)) - 1u));
                 const uint32_t ent0 = e0 + 8 * rank;
                 const uint64_t w = ent0 + 8 <= cap ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
                 const uint64_t vmask = valid_mask(nvalid, ent0);
@@ -461,21 +510,21 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
                 const uint32_t pzp = pz + 1 < RR ? plev[sx | sy | (spread3_u32(pz + 1) << 2)] : 0u;
                 Group g;
                 eval_group(w, pv, pxp, pyp, pzp, bf, g);
-                r0[(2 * py) * RR + px] = g.v[0] | (g.v[1] << 16);
-                r0[(2 * py + 1) * RR + px] = g.v[2] | (g.v[3] << 16);
-                r1[(2 * py) * RR + px] = g.v[4] | (g.v[5] << 16);
-                r1[(2 * py + 1) * RR + px] = g.v[6] | (g.v[7] << 16);
+                r0[(2 * py) * RR + px] = pack2<IT>(g.v[0], g.v[1]);
+                r0[(2 * py + 1) * RR + px] = pack2<IT>(g.v[2], g.v[3]);
+                r1[(2 * py) * RR + px] = pack2<IT>(g.v[4], g.v[5]);
+                r1[(2 * py + 1) * RR + px] = pack2<IT>(g.v[6], g.v[7]);
                 pdesc[k] = (uint16_t)g.pend;
                 anyp |= g.pend;
                 const uint64_t pmk = m_pal(w);
                 unsigned long long pk = ~0ull;
                 if (pmk) {
                     const int32_t ipq = B.ipb[rank];
-                    uint16_t* const p0 = reinterpret_cast<uint16_t*>(r0);
-                    uint16_t* const p1 = reinterpret_cast<uint16_t*>(r1);
+                    IT* const p0 = reinterpret_cast<IT*>(r0);
+                    IT* const p1 = reinterpret_cast<IT*>(r1);
                     pk = palette_children(w, pmk, ipq, B.plen, ent0, vmask, [&](uint32_t c, uint32_t idx) {
-                        uint16_t* pl = (c & 4) ? p1 : p0;
-                        pl[(2 * py + ((c >> 1) & 1)) * S2 + 2 * px + (c & 1)] = (uint16_t)idx;
+                        IT* pl = (c & 4) ? p1 : p0;
+                        pl[(2 * py + ((c >> 1) & 1)) * S2 + 2 * px + (c & 1)] = (IT)idx;
                     });
                 }
                 const uint64_t errs = m_op7(w) | (leaf ? (w >> 3) & ONES : 0ull);
@@ -484,9 +533,9 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
             }
         }
         __syncwarp();
-        const uint16_t* const pr = ring + ((2 * pz + 2) % 3) * PL;   // voxel plane 2pz-1
-        uint16_t* const p0 = ring + ((2 * pz) % 3) * PL;
-        uint16_t* const p1 = ring + ((2 * pz + 1) % 3) * PL;
+        const IT* const pr = ring + ((2 * pz + 2) % 3) * PL;   // voxel plane 2pz-1
+        IT* const p0 = ring + ((2 * pz) % 3) * PL;
+        IT* const p1 = ring + ((2 * pz + 1) % 3) * PL;
         // ---- chain rounds: child c <- child c | (1 << axis) of the -1 neighbour (ring)
         if (__any_sync(FULL, anyp != 0u)) {
 #pragma unroll
@@ -495,7 +544,7 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
                     const uint32_t k = k0 + lane;
                     const uint32_t pd = k < nl ? pdesc[k] : 0u;
                     if (pd) {
-                        const uint32_t i = plist[k] & 0xFFFFu;
+                        const uint32_t i = plist[k];
                         const uint32_t cx0 = 2 * (i % RR), cy0 = 2 * (i / RR);
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
@@ -503,8 +552,8 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
                             const uint32_t a1 = (pd >> (2 * c)) & 3u;
                             if (!a1) continue;
                             const uint32_t cx = cx0 + (c & 1), cy = cy0 + ((c >> 1) & 1);
-                            uint16_t* const dst = ((c & 4) ? p1 : p0) + cy * S2 + cx;
-                            uint16_t val;
+                            IT* const dst = ((c & 4) ? p1 : p0) + cy * S2 + cx;
+                            IT val;
                             if (a1 == 1u) val = dst[-1];
                             else if (a1 == 2u) val = dst[-(int)S2];
                             else val = ((c & 4) ? p0 : pr)[cy * S2 + cx];   // z - 1
@@ -519,14 +568,14 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
         for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
             const uint32_t k = k0 + lane;
             if (k < nl) {
-                const uint32_t i = plist[k] & 0xFFFFu;
+                const uint32_t i = plist[k];
                 const uint32_t px = i % RR, py = i / RR;
                 const uint32_t q = spread3_u32(px) | (spread3_u32(py) << 1) | sz;
-                const uint32_t* const q0 = reinterpret_cast<const uint32_t*>(p0);
-                const uint32_t* const q1 = reinterpret_cast<const uint32_t*>(p1);
+                const P2* const q0 = reinterpret_cast<const P2*>(p0);
+                const P2* const q1 = reinterpret_cast<const P2*>(p1);
                 const uint32_t a = q0[(2 * py) * RR + px], b = q0[(2 * py + 1) * RR + px];
                 const uint32_t c = q1[(2 * py) * RR + px], d = q1[(2 * py + 1) * RR + px];
-                const uint32_t vv[8] = {a & 0xFFFFu, a >> 16, b & 0xFFFFu, b >> 16, c & 0xFFFFu, c >> 16, d & 0xFFFFu, d >> 16};
+                const uint32_t vv[8] = {lo2<IT>(a), hi2<IT>(a), lo2<IT>(b), hi2<IT>(b), lo2<IT>(c), hi2<IT>(c), lo2<IT>(d), hi2<IT>(d)};
                 uint32_t lab[8];
                 const uint32_t l0 = __ldg(B.pal + vv[0]);
 #pragma unroll
@@ -542,23 +591,27 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
 
 }  // namespace wk
 
+#ifndef K2W_MINB
+#define K2W_MINB 10
+#endif
 #ifndef K2W_WPB
 #define K2W_WPB 2
 #endif
 constexpr int K2W_WARPS = K2W_WPB;
 
-template <int MODE, int LMAX>
-__global__ void __launch_bounds__(32 * K2W_WARPS) k2_warp(VolView V, Plan P, unsigned long long* counter) {
+template <int MODE, int LMAX, typename IT>
+__global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, Plan P, unsigned long long* counter) {
     using namespace wk;
-    constexpr WLayout Y = make_wlayout(LMAX);
+    constexpr WLayout Y = make_wlayout(LMAX, sizeof(IT));
+    constexpr bool WIDE = sizeof(IT) == 2;             // second pass: only bricks the u8 pass skipped
     extern __shared__ __align__(16) uint8_t wsm[];
     uint8_t* const base = wsm + (threadIdx.x >> 5) * Y.bytes;
-    uint16_t* const lev = reinterpret_cast<uint16_t*>(base + Y.lev);
+    IT* const lev = reinterpret_cast<IT*>(base + Y.lev);
     uint32_t* const mA = reinterpret_cast<uint32_t*>(base + Y.pm);
     uint32_t* const mB = reinterpret_cast<uint32_t*>(base + Y.cm);
     uint16_t* const wpre = reinterpret_cast<uint16_t*>(base + Y.wpre);
-    uint16_t* const ring = reinterpret_cast<uint16_t*>(base + Y.ring);
-    uint32_t* const plist = reinterpret_cast<uint32_t*>(base + Y.plist);
+    IT* const ring = reinterpret_cast<IT*>(base + Y.ring);
+    uint8_t* const plist = base + Y.plist;
     uint16_t* const pdesc = reinterpret_cast<uint16_t*>(base + Y.pdesc);
     uint16_t* const clist = reinterpret_cast<uint16_t*>(base + Y.clist);
     uint16_t* const cdesc = reinterpret_cast<uint16_t*>(base + Y.cdesc);
@@ -574,11 +627,12 @@ __global__ void __launch_bounds__(32 * K2W_WARPS) k2_warp(VolView V, Plan P, uns
         const uint64_t b = req_local(V, P, rr);
         B.t = req_lod(P, rr);
         B.N = V.N;
-        if (b >= V.nb || B.t > B.N) { if (lane == 0) put_result(P, rr, -1, 0, 0, 0, 0); continue; }
+        if (b >= V.nb || B.t > B.N) { if (!WIDE && lane == 0) put_result(P, rr, -1, 0, 0, 0, 0); continue; }
         B.n = B.N - B.t;
         if (B.t < B.N && B.n > LMAX) continue;          // served by the global-workspace kernel
-        B.out_m = MODE == OUT_MORTON ? P.out + P.dst[rr] : nullptr;
         B.plen = V.pal_len[b];
+        if (WIDE ? B.plen <= 256u : B.plen > 256u) continue;   // the other index width's pass
+        B.out_m = MODE == OUT_MORTON ? P.out + P.dst[rr] : nullptr;
         B.pal = V.palette + V.pal_off[b];
         if (MODE == OUT_RASTER) {
             const uint64_t gb = V.brick_begin + b;
@@ -634,21 +688,23 @@ __global__ void __launch_bounds__(32 * K2W_WARPS) k2_warp(VolView V, Plan P, uns
         uint32_t* cm = mB;
         bool failed = false;
         for (int j = 0; j + 1 < B.n; ++j) {      // parents at level N - j, children above the final level
-            const unsigned long long ek = coarse_level(B, j, lev, pm, cm, wpre, clist, cdesc, cur_c, ip_run, pdc, lane);
+            const unsigned long long ek = coarse_level<IT>(B, j, lev, pm, cm, wpre, clist, cdesc, cur_c, ip_run, pdc, lane);
             if (ek != ~0ull) { report_error(P, rr, B.Ec, B.capc, B.src, ek, false, lane); failed = true; break; }
             uint32_t* tmp = pm; pm = cm; cm = tmp;
         }
         if (failed) continue;
-        const uint16_t* plev = lev + wofs(B.n - 1);
+        const IT* plev = lev + wofs(B.n - 1);
+        // pdesc lives in whichever mask array is dead after the ping-pong (the layout aliases "cm")
+        uint16_t* const fdesc = Y.pdesc == Y.cm ? reinterpret_cast<uint16_t*>(cm) : pdesc;
         uint32_t& cur = B.t == 0 ? cur_d : cur_c;
         uint32_t& pdl = B.t == 0 ? pdd : pdc;
         unsigned long long ek;
         switch (B.n) {
-            case 1: ek = final_sweep<MODE, 1>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
-            case 2: ek = final_sweep<MODE, 2>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
-            case 3: ek = final_sweep<MODE, 4>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
-            case 4: ek = final_sweep<MODE, (LMAX >= 4 ? 8 : 1)>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
-            default: ek = final_sweep<MODE, (LMAX >= 5 ? 16 : 1)>(B, P, plev, pm, wpre, ring, plist, pdesc, cur, ip_run, pdl, lane); break;
+            case 1: ek = final_sweep<MODE, 1, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
+            case 2: ek = final_sweep<MODE, 2, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
+            case 3: ek = final_sweep<MODE, 4, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
+            case 4: ek = final_sweep<MODE, (LMAX >= 4 ? 8 : 1), IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
+            default: ek = final_sweep<MODE, (LMAX >= 5 ? 16 : 1), IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
         }
         if (ek != ~0ull) {
             if (B.t == 0) report_error(P, rr, B.Ed, B.capd, B.srd, ek, true, lane);
