@@ -47,7 +47,7 @@ __host__ __device__ constexpr uint32_t umax(uint32_t a, uint32_t b) { return a >
 //   pdesc : final level: their pending-chain descriptors (u16); aliases cm
 //   clist/cdesc : coarse levels: active list / descriptors (u16); alias the ring
 struct WLayout {
-    uint32_t lev, pm, cm, wpre, ring, plist, pdesc, clist, cdesc, bytes;   // byte offsets in one warp's slice
+    uint32_t lev, pm, cm, wpre, ring, plist, pdesc, clist, cdesc, spal, bytes;   // byte offsets in one warp's slice
 };
 __host__ __device__ constexpr WLayout make_wlayout(int L, uint32_t isz) {
     WLayout Y{};
@@ -76,6 +76,8 @@ __host__ __device__ constexpr WLayout make_wlayout(int L, uint32_t isz) {
         end = al16(end + 4 * cpar);
     }
     Y.cdesc = Y.clist + 2 * cpar;
+    Y.spal = end;                                         // u8 mode: the brick's palette (<= 256 labels)
+    if (isz == 1) end = al16(end + 1024);
     Y.bytes = end;
     return Y;
 }
@@ -213,7 +215,7 @@ __device__ __forceinline__ void eval_group(uint64_t w, uint32_t pv, uint32_t pxp
 }
 
 // Error key of one group (codec.py:396-457 order per entry: BAD_OP, LEAF_STOP, op-specific).
-__device__ __forceinline__ unsigned long long group_errkey(uint32_t ent0, uint64_t w, uint64_t vmask, bool leaf,
+__device__ __noinline__ unsigned long long group_errkey(uint32_t ent0, uint64_t w, uint64_t vmask, bool leaf,
                                                           uint32_t bn8) {
     unsigned long long k = ~0ull;
     const uint64_t bad = m_op7(w) & vmask;
@@ -260,11 +262,36 @@ struct Brick {
     uint32_t pitch, plane;
     uint32_t* out_m;
     bool al8, al16;
+    const uint32_t* spal;                // palette labels in shared memory (u8 mode)
+    bool al16r;                          // raster rows may be written as 16-byte vectors
     const uint8_t* Ec;  uint32_t capc;   // coarse entries, entry capacity (bytes)
     const uint8_t* Ed;  uint32_t capd;
     uint16_t* ipb;                       // per-warp scratch: palette base per final-level active parent
     csv_stream_result src, srd;
 };
+
+// label of a palette index (shared copy in u8 mode)
+template <typename IT>
+__device__ __forceinline__ uint32_t label_of(const Brick& B, uint32_t idx) {
+    return sizeof(IT) == 1 ? B.spal[idx] : __ldg(B.pal + idx);
+}
+
+// raster voxel (x, y, z) of the brick at LOD t, nullptr if cropped (container.py:465-468)
+__device__ __forceinline__ uint32_t* raster_xyz(const Raster& R, const Plan& P, uint32_t x, uint32_t y, uint32_t z) {
+    const int64_t gx = R.ox + x, gy = R.oy + y, gz = R.oz + z;
+    if (gz < P.z_begin || gz >= P.z_end || gy >= P.cy || gx >= P.cx) return nullptr;
+    return P.out + ((gz - P.z_begin) * P.cy + gy) * P.cx + gx;
+}
+
+// one voxel plane of the final level to HBM, per voxel with cropping (edge bricks)
+template <typename IT>
+__device__ __noinline__ void plane_rows_slow(Raster R, const Plan& P, const uint32_t* spal, const uint32_t* pal,
+                                             const IT* pl, uint32_t S2, uint32_t zz, int lane) {
+    for (uint32_t e = lane; e < S2 * S2; e += 32) {
+        uint32_t* const pp = raster_xyz(R, P, e % S2, e / S2, zz);
+        if (pp) *pp = sizeof(IT) == 1 ? spal[pl[e]] : __ldg(pal + pl[e]);
+    }
+}
 
 // Store the 8 children (palette labels) of final-level parent q = (px, py, pz).
 template <int MODE>
@@ -324,6 +351,12 @@ __device__ __noinline__ void report_error(const Plan& P, uint64_t r, const uint8
     }
     if (lane == 0) put_result(P, r, st, leaf ? 1 : 0, pos, 0, 0);
 }
+
+// pending-descriptor masks (2 bits per child) of the three chain rounds:
+// children 3,5,6 (targets: child 7), 1,2,4 (targets 3,5,6), 0 (targets 1,2,4)
+constexpr uint32_t kClass1 = (3u << 6) | (3u << 10) | (3u << 12);
+constexpr uint32_t kClass2 = (3u << 2) | (3u << 4) | (3u << 8);
+constexpr uint32_t kClass3 = 3u;
 
 // -1 / +1 neighbour along an axis of Morton index j (the axis' bits selected by M)
 __device__ __forceinline__ uint32_t morton_dec(uint32_t j, uint32_t M) { return (((j & M) - 1u) & M) | (j & ~M); }
@@ -399,22 +432,21 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
     __syncwarp();
     if (__any_sync(FULL, anyp != 0u)) {
         // rounds by decreasing popcount of the child index: targets are final
-#pragma unroll
-        for (int rd = 1; rd <= 3; ++rd) {
+#pragma unroll 1
+        for (int rd = 0; rd < 3; ++rd) {
+            const uint32_t cls = rd == 0 ? kClass1 : (rd == 1 ? kClass2 : kClass3);
+#pragma unroll 1
             for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
                 const uint32_t k = k0 + lane;
-                const uint32_t pd = k < nact ? pdesc[k] : 0u;
-                if (pd) {
-                    const uint32_t q = list[k];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        if (__popc(c) != 3 - rd) continue;
-                        const uint32_t a1 = (pd >> (2 * c)) & 3u;
-                        if (!a1) continue;
-                        const uint32_t M = a1 == 1 ? Cx : (a1 == 2 ? Cy : Cz);
-                        const uint32_t jj = (q << 3) | c;
-                        clev[jj] = clev[morton_dec(jj, M)];
-                    }
+                uint32_t m = k < nact ? (uint32_t)pdesc[k] & cls : 0u;
+                const uint32_t q = m ? list[k] : 0u;
+                while (m) {
+                    const uint32_t c = (uint32_t)(__ffs(m) - 1) >> 1;
+                    const uint32_t a1 = (m >> (2 * c)) & 3u;
+                    m &= ~(3u << (2 * c));
+                    const uint32_t M = a1 == 1 ? Cx : (a1 == 2 ? Cy : Cz);
+                    const uint32_t jj = (q << 3) | c;
+                    clev[jj] = clev[morton_dec(jj, M)];
                 }
             }
             __syncwarp();
@@ -480,8 +512,8 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
             const uint32_t bal = __ballot_sync(FULL, act);
             if (act) {
                 plist[nl + __popc(bal & lanemask_lt(lane))] = (uint8_t)i;
-            } else if (ok) {
-                const uint32_t l = __ldg(B.pal + pv);
+            } else if (MODE == OUT_MORTON && ok) {
+                const uint32_t l = label_of<IT>(B, pv);
                 const uint32_t lab[8] = {l, l, l, l, l, l, l, l};
                 store_children<MODE>(B, P, q, px, py, pz, lab);
             }
@@ -538,33 +570,55 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
         IT* const p1 = ring + ((2 * pz + 1) % 3) * PL;
         // ---- chain rounds: child c <- child c | (1 << axis) of the -1 neighbour (ring)
         if (__any_sync(FULL, anyp != 0u)) {
-#pragma unroll
-            for (int rd = 1; rd <= 3; ++rd) {
+#pragma unroll 1
+            for (int rd = 0; rd < 3; ++rd) {
+                const uint32_t cls = rd == 0 ? kClass1 : (rd == 1 ? kClass2 : kClass3);
+#pragma unroll 1
                 for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
                     const uint32_t k = k0 + lane;
-                    const uint32_t pd = k < nl ? pdesc[k] : 0u;
-                    if (pd) {
-                        const uint32_t i = plist[k];
-                        const uint32_t cx0 = 2 * (i % RR), cy0 = 2 * (i / RR);
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            if (__popc(c) != 3 - rd) continue;
-                            const uint32_t a1 = (pd >> (2 * c)) & 3u;
-                            if (!a1) continue;
-                            const uint32_t cx = cx0 + (c & 1), cy = cy0 + ((c >> 1) & 1);
-                            IT* const dst = ((c & 4) ? p1 : p0) + cy * S2 + cx;
-                            IT val;
-                            if (a1 == 1u) val = dst[-1];
-                            else if (a1 == 2u) val = dst[-(int)S2];
-                            else val = ((c & 4) ? p0 : pr)[cy * S2 + cx];   // z - 1
-                            *dst = val;
-                        }
+                    uint32_t m = k < nl ? (uint32_t)pdesc[k] & cls : 0u;
+                    const uint32_t i = m ? plist[k] : 0u;
+                    const uint32_t cx0 = 2 * (i % RR), cy0 = 2 * (i / RR);
+                    while (m) {
+                        const uint32_t c = (uint32_t)(__ffs(m) - 1) >> 1;
+                        const uint32_t a1 = (m >> (2 * c)) & 3u;
+                        m &= ~(3u << (2 * c));
+                        const uint32_t cx = cx0 + (c & 1), cy = cy0 + ((c >> 1) & 1);
+                        IT* const dst = ((c & 4) ? p1 : p0) + cy * S2 + cx;
+                        const IT* const src = a1 == 1u ? dst - 1 : (a1 == 2u ? dst - S2 : ((c & 4) ? p0 : pr) + cy * S2 + cx);
+                        *dst = *src;
                     }
                 }
                 __syncwarp();
             }
         }
-        // ---- active parents to HBM
+        if (MODE == OUT_RASTER) {
+            // ---- the plane pair to HBM as whole rows (each sector written once)
+#pragma unroll 1
+            for (int dz = 0; dz < 2; ++dz) {
+                const IT* const pl = dz ? p1 : p0;
+                const uint32_t zz = 2 * pz + dz;
+                if (S2 >= 4 && B.al16r) {
+                    uint32_t* const zb = B.R.base + zz * B.plane;
+                    for (uint32_t e = 4 * lane; e < PL; e += 128) {
+                        uint32_t v0, v1, v2, v3;
+                        if (sizeof(IT) == 1) {
+                            const uint32_t x = *reinterpret_cast<const uint32_t*>(pl + e);
+                            v0 = x & 0xFFu; v1 = (x >> 8) & 0xFFu; v2 = (x >> 16) & 0xFFu; v3 = x >> 24;
+                        } else {
+                            const uint2 x = *reinterpret_cast<const uint2*>(pl + e);
+                            v0 = x.x & 0xFFFFu; v1 = x.x >> 16; v2 = x.y & 0xFFFFu; v3 = x.y >> 16;
+                        }
+                        const uint4 lab = make_uint4(label_of<IT>(B, v0), label_of<IT>(B, v1), label_of<IT>(B, v2),
+                                                     label_of<IT>(B, v3));
+                        *reinterpret_cast<uint4*>(zb + (e / S2) * B.pitch + (e % S2)) = lab;
+                    }
+                } else {
+                    plane_rows_slow<IT>(B.R, P, B.spal, B.pal, pl, S2, zz, lane);
+                }
+            }
+        } else {
+        // ---- active parents to HBM (Morton: 8 children = one 32-byte sector)
         for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
             const uint32_t k = k0 + lane;
             if (k < nl) {
@@ -577,11 +631,11 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
                 const uint32_t c = q1[(2 * py) * RR + px], d = q1[(2 * py + 1) * RR + px];
                 const uint32_t vv[8] = {lo2<IT>(a), hi2<IT>(a), lo2<IT>(b), hi2<IT>(b), lo2<IT>(c), hi2<IT>(c), lo2<IT>(d), hi2<IT>(d)};
                 uint32_t lab[8];
-                const uint32_t l0 = __ldg(B.pal + vv[0]);
 #pragma unroll
-                for (int cc = 0; cc < 8; ++cc) lab[cc] = vv[cc] == vv[0] ? l0 : __ldg(B.pal + vv[cc]);
+                for (int cc = 0; cc < 8; ++cc) lab[cc] = label_of<IT>(B, vv[cc]);
                 store_children<MODE>(B, P, q, px, py, pz, lab);
             }
+        }
         }
         __syncwarp();
     }
@@ -634,6 +688,12 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         if (WIDE ? B.plen <= 256u : B.plen > 256u) continue;   // the other index width's pass
         B.out_m = MODE == OUT_MORTON ? P.out + P.dst[rr] : nullptr;
         B.pal = V.palette + V.pal_off[b];
+        if (sizeof(IT) == 1) {   // the palette (<= 256 labels) into the warp's slice
+            uint32_t* const sp = reinterpret_cast<uint32_t*>(base + Y.spal);
+            for (uint32_t i = lane; i < B.plen; i += 32) sp[i] = __ldg(B.pal + i);
+            B.spal = sp;
+            __syncwarp();
+        }
         if (MODE == OUT_RASTER) {
             const uint64_t gb = V.brick_begin + b;
             const int64_t side = 1ll << B.n;
@@ -646,6 +706,7 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
             B.pitch = (uint32_t)P.cx;
             B.plane = (uint32_t)(P.cx * P.cy);
             B.al8 = B.R.fast && (B.pitch & 1u) == 0u && (reinterpret_cast<uintptr_t>(B.R.base) & 7u) == 0u;
+            B.al16r = B.R.fast && (B.pitch & 3u) == 0u && (reinterpret_cast<uintptr_t>(B.R.base) & 15u) == 0u;
         } else {
             B.al16 = (reinterpret_cast<uintptr_t>(B.out_m) & 15u) == 0u;
         }
