@@ -300,8 +300,8 @@ __device__ __forceinline__ void store_children(const Brick& B, const Plan& P, ui
     if (MODE == OUT_MORTON) {
         uint32_t* g = B.out_m + 8ull * q;
         if (B.al16) {
-            reinterpret_cast<uint4*>(g)[0] = make_uint4(lab[0], lab[1], lab[2], lab[3]);
-            reinterpret_cast<uint4*>(g)[1] = make_uint4(lab[4], lab[5], lab[6], lab[7]);
+            __stcs(reinterpret_cast<uint4*>(g), make_uint4(lab[0], lab[1], lab[2], lab[3]));   // streaming: keep
+            __stcs(reinterpret_cast<uint4*>(g) + 1, make_uint4(lab[4], lab[5], lab[6], lab[7]));   // entries in L2
         } else {
 #pragma unroll
             for (int c = 0; c < 8; ++c) g[c] = lab[c];
@@ -611,7 +611,7 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
                         }
                         const uint4 lab = make_uint4(label_of<IT>(B, v0), label_of<IT>(B, v1), label_of<IT>(B, v2),
                                                      label_of<IT>(B, v3));
-                        *reinterpret_cast<uint4*>(zb + (e / S2) * B.pitch + (e % S2)) = lab;
+                        __stcs(reinterpret_cast<uint4*>(zb + (e / S2) * B.pitch + (e % S2)), lab);   // evict-first
                     }
                 } else {
                     plane_rows_slow<IT>(B.R, P, B.spal, B.pal, pl, S2, zz, lane);
