@@ -330,6 +330,7 @@ def run_ours(args, world, rank, local):
     k2_bytes = entries + pal_b + 44 * n_b + 4 * voxels_rank
     del ent, offs, sres
     dom = ("k2_replay", k2_ms, k2_bytes) if k2_ms >= k1_ms else ("k1_streams", k1_ms, k1_bytes)
+    long_pal = int(d["palette_len"].max()) > 256 if n_b else False      # K2w runs a second (u16) pass
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -337,7 +338,7 @@ def run_ours(args, world, rank, local):
     except Exception:
         pass
     achieved = dom[2] / (dom[1] * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+    roofline = {"bound": "hbm", "kernel": "k2_warp" if dom[0] == "k2_replay" else dom[0], "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                 "algorithmic_bytes": dom[2], "kernel_ms": dom[1]}
     step_gbs = step_bytes / (ms_rank * 1e-3) / 1e9
@@ -356,7 +357,7 @@ def run_ours(args, world, rank, local):
                           "algorithmic_bytes": step_bytes, "bytes_per_voxel": step_bytes / voxels_rank},
         "stages_ms": {"plan": plan_ms, "k1_streams": k1_ms, "k2_replay": k2_ms},
         "clocks": clk,
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": (7 if long_pal else 6) * args.steps,   # sizes, 3 scan, K1, K2w (+ u16 K2w)
         "setup_s": {"synth": t_synth, "encode": t_enc},
     }
     # ---- config 4: batched random-access decode into a device brick pool
