@@ -369,7 +369,9 @@ def run_ours(args, world, rank, local):
         cache.begin_frame()
         for br, l in reqs:
             cache.mark_used(br, l)
+        tp0 = time.perf_counter()
         placed, live = cache.plan_frame(reqs)
+        host_plan_ms = (time.perf_counter() - tp0) * 1e3
         arr = np.asarray(live, dtype=np.int64)
         bricks = torch.from_numpy(arr[:, 0].astype(np.int32)).to(dev)
         lods = torch.from_numpy(arr[:, 1].astype(np.uint8)).to(dev)
@@ -394,8 +396,48 @@ def run_ours(args, world, rank, local):
                                 "workload": "config 4: camera (1024,1024,-64) +z, H=1080, fov pi/3, "
                                             "desired_lods, 65,536 nearest bricks -> BrickCache plan -> one "
                                             "csv_decode_bricks batch into an 8 GiB device pool"}
-        full.close()
+        # the same frame with the residency bookkeeping on the GPU too:
+        # device LOD selection + DeviceBrickCache (evict / free stacks / carve, atomics) + batched decode
         del cache
+        torch.cuda.empty_cache()
+        dcache = p.DeviceBrickCache(gx * gy * gz, BRICK_LOG2, pool_bytes=8 << 30, device=dev)
+        rb = torch.from_numpy(np.array([r[0] for r in reqs], np.int32)).to(dev)
+        rl = torch.from_numpy(np.array([r[1] for r in reqs], np.uint8)).to(dev)
+        none_b = torch.empty(0, dtype=torch.int32, device=dev)
+        none_l = torch.empty(0, dtype=torch.uint8, device=dev)
+        cam = p.Camera(position=(1024.0, 1024.0, -64.0), fov=math.pi / 3, width=1920, height=1080)
+        dl = p.desired_lods_device(full, cam)
+        assert torch.equal(dl[rb.long()], rl), "device LODs differ from the restated desired_lods"
+
+        def frame():
+            p.desired_lods_device(full, cam, out=dl)
+            dcache.begin_frame()
+            dcache.mark_used(rb, rl)
+            return dcache.end_frame_assign(rb, rl, full)
+
+        def evict_all():
+            dcache.begin_frame()
+            dcache.end_frame_assign(none_b, none_l, full)
+
+        for _ in range(max(1, args.warmup)):
+            evict_all()
+            frame()
+        ftimes = []
+        for _ in range(args.steps):
+            evict_all()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            nplaced = frame()
+            torch.cuda.synchronize()
+            ftimes.append(time.perf_counter() - t0)
+        fs = statistics.median(ftimes)
+        line["random_brick"]["device_frame"] = {
+            "value": cvox / fs / 1e9, "unit": "GVoxel/s", "ms_per_frame": fs * 1e3, "placed": nplaced,
+            "host_plan_ms": host_plan_ms,   # the reference-style serial bookkeeping of the same frame (cache.py)
+            "path": "desired_lods_device + DeviceBrickCache begin_frame/mark_used/end_frame_assign "
+                    "(want, free stacks, carve, batched K1+K2w decode); wall clock, median"}
+        dcache.close()
+        full.close()
     # ---- config 5: time series encode + decode (2 timesteps = one GPU's share of 16 over 8 GPUs)
     if not args.no_cache and not args.profile and world == 1 and args.workload == "config3" and not args.zlayers:
         line["timeseries"] = timeseries_leg(p, torch, dev, stream)

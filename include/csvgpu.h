@@ -36,6 +36,7 @@ extern "C" {
 #define CSV_E_CUDA (-2)     /* CUDA runtime error */
 #define CSV_E_NOMEM (-3)    /* device allocation failed */
 #define CSV_E_FORMAT (-4)   /* malformed container header */
+#define CSV_E_CAPACITY (-5) /* brick cache: the visible set does not fit the pool (CacheCapacityError) */
 
 /* Per-brick status codes: 0..7 as codec.py:280-287, plus CSV_ST_EMPTY_PALETTE
  * for codec.py:510-511 ("empty palette"). */
@@ -201,7 +202,57 @@ int csv_encoded_free(csv_encoded* enc);
 int csv_synth_voronoi(uint32_t* d_out, int64_t X, int64_t Y, int64_t Z, int cells_per_axis, uint32_t seed,
                       int membrane, double drift, uint32_t drift_seed, uintptr_t stream);
 
+/* ---------------------------------------------------------------- frame bookkeeping
+ * Device restatements of the steps around the batched cache decode. */
+
+/* desired_lods (render.py:145-158): per brick of the volume's range,
+ * clip(ceil(log2(max(1, |centre - pos| * 2 * tan_half_fov / height))), 0, N).
+ * tan_half_fov = tan(fov / 2) computed by the caller (math.tan, as the reference). */
+int csv_desired_lods(csv_volume* vol, double px, double py, double pz, double tan_half_fov, double height,
+                     uint8_t* d_lod, uintptr_t stream);
+
+/* visibility_mask (render.py:174-187): brick visible iff a palette entry in
+ * [pal_off_i, pal_off_{i+1}) (numpy add.reduceat semantics) has alpha > 0;
+ * alpha from the sorted override labels d_tf_labels / d_tf_alpha (n_tf), else
+ * default_alpha.  palette_total = entries of the uploaded palette slice. */
+int csv_visibility_mask(csv_volume* vol, uint64_t palette_total, const uint32_t* d_tf_labels,
+                        const double* d_tf_alpha, uint32_t n_tf, double default_alpha, uint8_t* d_vis,
+                        uintptr_t stream);
+
+/* Device-resident brick cache: BrickCache (cache.py:49-195) with the residency
+ * state in device memory and end_frame_assign done by bulk kernels (per-size-
+ * class free stacks with atomics; deterministic brick-order rebuild on pool
+ * exhaustion, CSV_E_CAPACITY when even that does not fit).  The pool (u32,
+ * pool_elements * 8 labels) is owned by the caller. */
+typedef struct csv_cache csv_cache;
+int csv_cache_create(int device, uint64_t num_bricks, int brick_log2, uint64_t pool_elements, csv_cache** cache);
+int csv_cache_free(csv_cache* cache);
+/* begin_frame (cache.py:78-80): every usage flag <- invisible (-1). */
+int csv_cache_begin_frame(csv_cache* cache, uintptr_t stream);
+/* mark_used (cache.py:82-89) for n (brick, lod) pairs. */
+int csv_cache_mark_used(csv_cache* cache, const uint32_t* d_bricks, const uint8_t* d_lods, uint64_t n,
+                        uintptr_t stream);
+/* end_frame_assign (cache.py:139-170) + the batched decode of every placement
+ * into d_pool (K1 + K2w, as csv_decode_bricks).  d_res receives one csv_result
+ * per placement (capacity >= number of bricks); *placed = placements; *rebuilt = 1
+ * if the pool was rebuilt.  Synchronises the stream (the placement count sizes
+ * the decode launch). */
+int csv_cache_assign(csv_cache* cache, csv_volume* vol, const uint32_t* d_bricks, const uint8_t* d_lods, uint64_t n,
+                     uint32_t* d_pool, csv_result* d_res, uint64_t* placed, int* rebuilt, uintptr_t stream);
+/* Device pointers of the residency state: block_start (i64, base elements),
+ * resident LOD (i8, -1 = not resident), usage (i8), last frame's fill list. */
+int csv_cache_state(csv_cache* cache, int64_t** d_block_start, int8_t** d_resident, int8_t** d_usage,
+                    uint32_t** d_fill_brick, uint8_t** d_fill_lod, uint64_t** d_fill_dst);
+/* Host copies of block_start (i64) and resident LOD (i8), num_bricks entries each. */
+int csv_cache_read_state(csv_cache* cache, int64_t* block_start, int8_t* resident);
+/* Counters: {top, evictions, rebuilds, decodes, decoded_bytes, last_placed, 0, 0}. */
+int csv_cache_counters(csv_cache* cache, uint64_t* out8);
+/* Free-stack heights per size class (brick_log2 entries). */
+int csv_cache_stack_heights(csv_cache* cache, int64_t* out_n);
+
+
 #ifdef __cplusplus
 }
 #endif
+
 #endif /* CSVGPU_H */

@@ -25,6 +25,9 @@ EXPORTS = (
     "csv_encode_volume", "csv_encoded_info", "csv_encoded_device_ptrs", "csv_encoded_copy_to_host",
     "csv_encoded_free", "csv_synth_voronoi", "csv_volume_set_timing", "csv_volume_get_timing",
     "csv_volume_op_counts", "csv_decode_volume_range", "csv_volume_create_deferred", "csv_volume_upload",
+    "csv_desired_lods", "csv_visibility_mask", "csv_cache_create", "csv_cache_free", "csv_cache_begin_frame",
+    "csv_cache_mark_used", "csv_cache_assign", "csv_cache_state", "csv_cache_counters", "csv_cache_stack_heights",
+    "csv_cache_read_state",
 )
 
 
@@ -89,6 +92,29 @@ def lib():
         L.csv_volume_set_timing.argtypes = [P, I]
         L.csv_volume_get_timing.restype = I
         L.csv_volume_get_timing.argtypes = [P, P]
+        D = ctypes.c_double
+        L.csv_desired_lods.restype = I
+        L.csv_desired_lods.argtypes = [P, D, D, D, D, D, P, UP]
+        L.csv_visibility_mask.restype = I
+        L.csv_visibility_mask.argtypes = [P, U64, P, P, ctypes.c_uint32, D, P, UP]
+        L.csv_cache_create.restype = I
+        L.csv_cache_create.argtypes = [I, U64, I, U64, P]
+        L.csv_cache_free.restype = I
+        L.csv_cache_free.argtypes = [P]
+        L.csv_cache_begin_frame.restype = I
+        L.csv_cache_begin_frame.argtypes = [P, UP]
+        L.csv_cache_mark_used.restype = I
+        L.csv_cache_mark_used.argtypes = [P, P, P, U64, UP]
+        L.csv_cache_assign.restype = I
+        L.csv_cache_assign.argtypes = [P, P, P, P, U64, P, P, P, P, UP]
+        L.csv_cache_state.restype = I
+        L.csv_cache_state.argtypes = [P, P, P, P, P, P, P]
+        L.csv_cache_read_state.restype = I
+        L.csv_cache_read_state.argtypes = [P, P, P]
+        L.csv_cache_counters.restype = I
+        L.csv_cache_counters.argtypes = [P, P]
+        L.csv_cache_stack_heights.restype = I
+        L.csv_cache_stack_heights.argtypes = [P, P]
         _lib = L
     return _lib
 

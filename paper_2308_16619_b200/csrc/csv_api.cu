@@ -306,6 +306,11 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
     return CSV_OK;
 }
 
+namespace csv {
+const VolView& volume_view(const csv_volume* v) { return v->V; }
+int volume_device(const csv_volume* v) { return v->device; }
+}  // namespace csv
+
 // ---------------------------------------------------------------------------- exported API
 extern "C" {
 

@@ -91,6 +91,7 @@ class GpuVolume:
                 rc = L.csv_volume_create_device(
                     self.device.index, _ptr(head), dp, self.brick_begin, self.brick_end,
                     pp, palette_base, pn, cp, coarse_base, cn, xp, detail_base, xn, sh, ctypes.byref(handle))
+                self.palette_entries = int(pn)
             elif deferred:
                 # blobs allocated now, filled by upload(); palette/coarse/detail are their lengths
                 d = np.ascontiguousarray(directory).view(np.uint8)
@@ -99,6 +100,7 @@ class GpuVolume:
                     self.device.index, _ptr(head), _ptr(d), self.brick_begin, self.brick_end,
                     palette_base, int(palette), coarse_base, int(coarse), detail_base, int(detail), sh,
                     ctypes.byref(handle))
+                self.palette_entries = int(palette)
             else:
                 d = np.ascontiguousarray(directory).view(np.uint8)
                 pal = np.ascontiguousarray(palette, dtype="<u4")
@@ -109,6 +111,7 @@ class GpuVolume:
                     self.device.index, _ptr(head), _ptr(d), self.brick_begin, self.brick_end,
                     _ptr(pal), palette_base, pal.size, _ptr(cb), coarse_base, cb.size,
                     _ptr(db), detail_base, db.size, sh, ctypes.byref(handle))
+                self.palette_entries = int(pal.size)
             _lib.check(rc)
         self._h = handle
         dims = (ctypes.c_int64 * 3)()
