@@ -115,6 +115,14 @@ int csv_volume_create_deferred(int device, const uint8_t* head120, const uint8_t
                                csv_volume** vol);
 int csv_volume_upload(csv_volume* vol, int blob, const void* host, uint64_t offset, uint64_t nbytes, uintptr_t stream);
 
+/* Cold detail (render.py:782-832, container.py:148-159): for a volume created
+ * without its detail blob, make the n staged bricks' level-0 streams readable
+ * from d_stage (brick d_bricks[i] at byte d_offs[i], d_lens[i] bytes); every
+ * other brick has no detail stream until staged again.  d_stage is borrowed
+ * and needs 64 readable bytes past stage_len. */
+int csv_volume_stage_detail(csv_volume* vol, const uint32_t* d_bricks, const uint64_t* d_offs, const uint32_t* d_lens,
+                            uint64_t n, const uint8_t* d_stage, uint64_t stage_len, uintptr_t stream);
+
 int csv_volume_free(csv_volume* vol);
 
 /* Full-volume decode at LOD t into a raster (Z,Y,X) u32 slab: replaces
@@ -239,10 +247,19 @@ int csv_cache_mark_used(csv_cache* cache, const uint32_t* d_bricks, const uint8_
  * the decode launch). */
 int csv_cache_assign(csv_cache* cache, csv_volume* vol, const uint32_t* d_bricks, const uint8_t* d_lods, uint64_t n,
                      uint32_t* d_pool, csv_result* d_res, uint64_t* placed, int* rebuilt, uintptr_t stream);
+/* The two halves of csv_cache_assign: plan (residency only; the fill list is
+ * then readable through csv_cache_state, *placed entries) and the batched
+ * decode of that fill list -- so a caller can stage cold detail streams for
+ * the LOD-0 placements in between (render.py:876-885). */
+int csv_cache_plan(csv_cache* cache, const uint32_t* d_bricks, const uint8_t* d_lods, uint64_t n, uint64_t* placed,
+                   int* rebuilt, uintptr_t stream);
+int csv_cache_decode_fills(csv_cache* cache, csv_volume* vol, uint32_t* d_pool, csv_result* d_res, uintptr_t stream);
 /* Device pointers of the residency state: block_start (i64, base elements),
  * resident LOD (i8, -1 = not resident), usage (i8), last frame's fill list. */
 int csv_cache_state(csv_cache* cache, int64_t** d_block_start, int8_t** d_resident, int8_t** d_usage,
                     uint32_t** d_fill_brick, uint8_t** d_fill_lod, uint64_t** d_fill_dst);
+/* Host copy of the last plan's fill list: up to cap (brick, lod) pairs; *n = placements. */
+int csv_cache_read_fills(csv_cache* cache, uint32_t* bricks, uint8_t* lods, uint64_t cap, uint64_t* n);
 /* Host copies of block_start (i64) and resident LOD (i8), num_bricks entries each. */
 int csv_cache_read_state(csv_cache* cache, int64_t* block_start, int8_t* resident);
 /* Counters: {top, evictions, rebuilds, decodes, decoded_bytes, last_placed, 0, 0}. */

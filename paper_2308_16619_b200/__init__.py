@@ -10,6 +10,7 @@ from .cache import BrickCache, CacheStats, DeviceBrickCache
 from .codec import BrickEncoding, decode_brick, decode_brick_entropy, decode_root, iter_operations
 from .container import (CompressionConfig, CsvContainer, VolumeMeta, decompress_volume,
                         decompress_volume_device, stats)
+from .detail import DetailStore, DeviceDetailStream
 from .device import GpuVolume
 from .frame import Camera, TransferFunction, desired_lods, desired_lods_device, visibility_mask, visibility_mask_device
 from .encode import GpuEncoded, compress_volume, compress_volume_device, synth_voronoi
@@ -21,7 +22,7 @@ from .rans import FrequencyTable, TablePair, build_frequency_tables, quantize_co
 __version__ = "0.1.0"
 
 __all__ = [
-    "BrickCache", "BrickConfig", "Camera", "DeviceBrickCache", "TransferFunction", "desired_lods",
+    "BrickCache", "BrickConfig", "DetailStore", "DeviceDetailStream", "Camera", "DeviceBrickCache", "TransferFunction", "desired_lods",
     "desired_lods_device", "visibility_mask", "visibility_mask_device", "BrickEncoding", "CacheCapacityError", "CacheStats", "CompressionConfig",
     "ConfigError", "CorruptStreamError", "CsvContainer", "CsvolError", "EncodabilityError", "FrequencyTable",
     "GpuEncoded", "GpuVolume", "compress_volume", "compress_volume_device", "synth_voronoi", "IngestionError", "NodeCoord", "TablePair", "VolumeMeta", "build_frequency_tables",

@@ -27,7 +27,8 @@ EXPORTS = (
     "csv_volume_op_counts", "csv_decode_volume_range", "csv_volume_create_deferred", "csv_volume_upload",
     "csv_desired_lods", "csv_visibility_mask", "csv_cache_create", "csv_cache_free", "csv_cache_begin_frame",
     "csv_cache_mark_used", "csv_cache_assign", "csv_cache_state", "csv_cache_counters", "csv_cache_stack_heights",
-    "csv_cache_read_state",
+    "csv_cache_read_state", "csv_cache_plan", "csv_cache_decode_fills", "csv_volume_stage_detail",
+    "csv_cache_read_fills",
 )
 
 
@@ -109,6 +110,14 @@ def lib():
         L.csv_cache_assign.argtypes = [P, P, P, P, U64, P, P, P, P, UP]
         L.csv_cache_state.restype = I
         L.csv_cache_state.argtypes = [P, P, P, P, P, P, P]
+        L.csv_cache_plan.restype = I
+        L.csv_cache_plan.argtypes = [P, P, P, U64, P, P, UP]
+        L.csv_cache_decode_fills.restype = I
+        L.csv_cache_decode_fills.argtypes = [P, P, P, P, UP]
+        L.csv_volume_stage_detail.restype = I
+        L.csv_volume_stage_detail.argtypes = [P, P, P, P, U64, P, U64, UP]
+        L.csv_cache_read_fills.restype = I
+        L.csv_cache_read_fills.argtypes = [P, P, P, U64, P]
         L.csv_cache_read_state.restype = I
         L.csv_cache_read_state.argtypes = [P, P, P]
         L.csv_cache_counters.restype = I

@@ -218,11 +218,15 @@ class CsvContainer:
         return c
 
     # -- device residency --------------------------------------------------------
-    def to_device(self, device=None, brick_range: tuple[int, int] | None = None):
-        """Upload (a whole-bz-layer brick range of) this container: a GpuVolume."""
+    def to_device(self, device=None, brick_range: tuple[int, int] | None = None, cold_detail: bool = False):
+        """Upload (a whole-bz-layer brick range of) this container: a GpuVolume.
+
+        With ``cold_detail`` (or when the detail section stayed on disk,
+        ``open(..., detail_cold=True)``) the detail blob is not uploaded; level-0
+        decodes then read streams staged per frame by a DeviceDetailStream.
+        """
         from .device import GpuVolume
-        if self.detail_blob is None:
-            raise ConfigError("device upload needs the detail section in memory")
+        cold_detail = cold_detail or self.detail_blob is None
         b0, b1 = brick_range if brick_range is not None else (0, self.meta.brick_count)
         d = self.directory[b0:b1]
         if b1 > b0:
@@ -234,9 +238,10 @@ class CsvContainer:
             d1 = int((d["detail_off"].astype(np.int64) + d["detail_bytes"]).max())
         else:
             p0 = p1 = c0 = c1 = d0 = d1 = 0
-        p1, c1, d1 = min(p1, self.palette_blob.size), min(c1, self.coarse_blob.size), min(d1, self.detail_blob.size)
+        p1, c1 = min(p1, self.palette_blob.size), min(c1, self.coarse_blob.size)
+        det = np.zeros(0, np.uint8) if cold_detail else self.detail_blob[d0:max(d0, min(d1, self.detail_blob.size))]
         return GpuVolume(self.head_bytes(), d, self.palette_blob[p0:max(p0, p1)], self.coarse_blob[c0:max(c0, c1)],
-                         self.detail_blob[d0:max(d0, d1)], brick_begin=b0, brick_end=b1, palette_base=p0,
+                         det, brick_begin=b0, brick_end=b1, palette_base=p0,
                          coarse_base=c0, detail_base=d0, device=device)
 
 

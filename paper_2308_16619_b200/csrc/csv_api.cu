@@ -121,6 +121,19 @@ __global__ void k_region_stats(VolView V, unsigned long long* total, unsigned lo
     }
 }
 
+// Cold detail (render.py:782-832): point the staged bricks' detail streams at
+// the frame's staging buffer; every other brick has no detail until staged.
+__global__ void k_stage_detail(uint64_t* d_off, uint32_t* d_bytes, uint64_t brick_begin, uint64_t nb,
+                               const uint32_t* bricks, const uint64_t* offs, const uint32_t* lens, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t b = (uint64_t)bricks[i] - brick_begin;
+    if (b < nb) {
+        d_off[b] = offs[i];
+        d_bytes[b] = lens[i];
+    }
+}
+
 // ---------------------------------------------------------------------------- helpers
 static int parse_head(const uint8_t* h, csv_volume* v, uint32_t* dtab_host) {
     if (memcmp(h, "CSV1", 4) != 0) return fail(CSV_E_FORMAT, "bad magic");
@@ -350,6 +363,40 @@ int csv_volume_upload(csv_volume* vol, int blob, const void* host, uint64_t offs
     CUDA_TRY(cudaSetDevice(vol->device));
     uint8_t* base = blob == 0 ? (uint8_t*)vol->V.palette : (blob == 1 ? (uint8_t*)vol->V.coarse : (uint8_t*)vol->V.detail);
     CUDA_TRY(cudaMemcpyAsync(base + offset, host, nbytes, cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream)));
+    return CSV_OK;
+}
+
+int csv_volume_stage_detail(csv_volume* vol, const uint32_t* d_bricks, const uint64_t* d_offs, const uint32_t* d_lens,
+                            uint64_t n, const uint8_t* d_stage, uint64_t stage_len, uintptr_t stream) {
+    if (!vol || (n && (!d_bricks || !d_offs || !d_lens || !d_stage))) return fail(CSV_E_ARG, "null argument");
+    CUDA_TRY(cudaSetDevice(vol->device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    uint32_t* dbytes = const_cast<uint32_t*>(vol->V.d_bytes);
+    uint64_t* doff = const_cast<uint64_t*>(vol->V.d_off);
+    if (vol->V.nb) {
+        CUDA_TRY(cudaMemsetAsync(dbytes, 0, vol->V.nb * 4, st));
+        CUDA_TRY(cudaMemsetAsync(doff, 0, vol->V.nb * 8, st));
+    }
+    vol->V.detail = d_stage;
+    vol->blob_cap[2] = stage_len;
+    if (n) {
+        k_stage_detail<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(doff, dbytes, vol->V.brick_begin, vol->V.nb, d_bricks,
+                                                                   d_offs, d_lens, n);
+        CUDA_TRY(cudaGetLastError());
+    }
+    if (!vol->V.entropy && vol->V.nb) {   // raw streams: entry regions depend on the stream bytes
+        unsigned long long* stats = nullptr;
+        CUDA_TRY(cudaMalloc(&stats, 24));
+        cudaMemsetAsync(stats, 0, 24, st);
+        k_region_stats<<<(unsigned)((vol->V.nb + 255) / 256), 256, 0, st>>>(vol->V, stats, stats + 1);
+        unsigned long long hs[3] = {0, 0, 0};
+        cudaMemcpyAsync(hs, stats, 24, cudaMemcpyDeviceToHost, st);
+        cudaError_t ce = cudaStreamSynchronize(st);
+        cudaFree(stats);
+        if (ce != cudaSuccess) return fail(CSV_E_CUDA, "stage: %s", cudaGetErrorString(ce));
+        vol->region_total_t0 = std::max<uint64_t>(vol->region_total_t0, hs[0]);
+        vol->region_max_t0 = std::max<uint64_t>(vol->region_max_t0, hs[1]);
+    }
     return CSV_OK;
 }
 

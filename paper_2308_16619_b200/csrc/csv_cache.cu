@@ -327,6 +327,10 @@ int csv_cache_mark_used(csv_cache* c, const uint32_t* d_bricks, const uint8_t* d
     return CSV_OK;
 }
 
+int csv_cache_plan(csv_cache* c, const uint32_t* d_bricks, const uint8_t* d_lods, uint64_t n, uint64_t* placed,
+                   int* rebuilt, uintptr_t stream);
+int csv_cache_decode_fills(csv_cache* c, csv_volume* vol, uint32_t* d_pool, csv_result* d_res, uintptr_t stream);
+
 // One frame's assignment + batched decode into d_pool.  *placed receives the
 // number of bricks decoded; *rebuilt is 1 when the pool was rebuilt.
 int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, const uint8_t* d_lod,
@@ -334,7 +338,26 @@ int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, cons
 
 int csv_cache_assign(csv_cache* c, csv_volume* vol, const uint32_t* d_bricks, const uint8_t* d_lods, uint64_t n,
                      uint32_t* d_pool, csv_result* d_res, uint64_t* placed, int* rebuilt, uintptr_t stream) {
-    if (!c || !vol || !d_pool || (n && (!d_bricks || !d_lods))) return cfail(CSV_E_ARG, "null argument");
+    const int rc = csv_cache_plan(c, d_bricks, d_lods, n, placed, rebuilt, stream);
+    if (rc) return rc;
+    return csv_cache_decode_fills(c, vol, d_pool, d_res, stream);
+}
+
+int csv_cache_decode_fills(csv_cache* c, csv_volume* vol, uint32_t* d_pool, csv_result* d_res, uintptr_t stream) {
+    if (!c || !vol || !d_pool) return cfail(CSV_E_ARG, "null argument");
+    const uint64_t nfill = c->last_placed;
+    if (nfill) {
+        const int rc = csv_decode_bricks(vol, nfill, c->C.fill_brick, c->C.fill_lod, c->C.fill_dst, d_pool, d_res, stream);
+        if (rc) return rc;
+        c->decodes += nfill;
+        c->decoded_bytes += c->h_ctr[C_FBYTES];
+    }
+    return CSV_OK;
+}
+
+int csv_cache_plan(csv_cache* c, const uint32_t* d_bricks, const uint8_t* d_lods, uint64_t n, uint64_t* placed,
+                   int* rebuilt, uintptr_t stream) {
+    if (!c || (n && (!d_bricks || !d_lods))) return cfail(CSV_E_ARG, "null argument");
     CTRY(cudaSetDevice(c->device));
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     CacheView& C = c->C;
@@ -379,12 +402,6 @@ int csv_cache_assign(csv_cache* c, csv_volume* vol, const uint32_t* d_bricks, co
     const uint64_t nfill = c->h_ctr[C_NFILL];
     if (placed) *placed = nfill;
     c->last_placed = nfill;
-    if (nfill) {
-        const int rc = csv_decode_bricks(vol, nfill, C.fill_brick, C.fill_lod, C.fill_dst, d_pool, d_res, stream);
-        if (rc) return rc;
-        c->decodes += nfill;
-        c->decoded_bytes += c->h_ctr[C_FBYTES];
-    }
     return CSV_OK;
 }
 
@@ -400,6 +417,20 @@ int csv_cache_state(csv_cache* c, int64_t** d_block_start, int8_t** d_resident, 
     if (d_fill_brick) *d_fill_brick = c->C.fill_brick;
     if (d_fill_lod) *d_fill_lod = c->C.fill_lod;
     if (d_fill_dst) *d_fill_dst = c->C.fill_dst;
+    return CSV_OK;
+}
+
+// Host copy of the last plan's fill list (brick, lod), up to cap entries; returns the count in *n.
+int csv_cache_read_fills(csv_cache* c, uint32_t* bricks, uint8_t* lods, uint64_t cap, uint64_t* n) {
+    if (!c || !n || (cap && (!bricks || !lods))) return cfail(CSV_E_ARG, "null argument");
+    CTRY(cudaSetDevice(c->device));
+    CTRY(cudaDeviceSynchronize());
+    const uint64_t k = c->last_placed < cap ? c->last_placed : cap;
+    if (k) {
+        CTRY(cudaMemcpy(bricks, c->C.fill_brick, k * 4, cudaMemcpyDeviceToHost));
+        CTRY(cudaMemcpy(lods, c->C.fill_lod, k, cudaMemcpyDeviceToHost));
+    }
+    *n = c->last_placed;
     return CSV_OK;
 }
 

@@ -1,0 +1,128 @@
+"""Cold-detail streaming for the cache decode.
+
+The reference keeps a container's detail section (the level-0 streams, the
+bulk of the bytes) on disk and fetches at most ``budget_bytes`` of requested
+streams per frame; bricks whose stream did not fit decode at level 1 this
+frame (DetailStore, render.py:782-832; cold reads, container.py:148-159).
+
+`DetailStore` is that planner, unchanged.  `DeviceDetailStream` adds the GPU
+side: the streams a frame's level-0 placements need (fetched ones from
+``hot``, the rest read synchronously like FrameLoop._decode, render.py:876-885)
+are packed into a pinned host buffer, copied to a device staging buffer in one
+asynchronous H2D transfer, and pointed at by the volume's directory
+(csv_volume_stage_detail) right before the batched decode.  The device volume
+itself never holds the detail blob.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+
+class DetailStore:
+    """Budgeted access to the cold detail section of a container (render.py:782-832)."""
+
+    def __init__(self, container, budget_bytes: int = 8 << 20):
+        self.container = container
+        self.budget_bytes = budget_bytes
+        self.hot: dict[int, np.ndarray] = {}
+        self.fetched_bytes_total = 0
+        self.deferred_last_frame = 0
+        self.fallback_log: list[tuple[int, int]] = []  # (frame, brick)
+        self._frame = 0
+
+    def plan(self, requests) -> list[tuple[int, int]]:
+        """Fetch detail for level-0 requests within budget; downgrade the rest to level 1."""
+        spent = 0
+        deferred = 0
+        adjusted: list[tuple[int, int]] = []
+        for brick, lod in sorted(set(requests)):
+            if lod != 0:
+                adjusted.append((brick, lod))
+                continue
+            size = self.container.detail_size(brick)
+            if size == 0 or brick in self.hot:
+                adjusted.append((brick, 0))
+                continue
+            if spent + size <= self.budget_bytes:
+                self.hot[brick] = self.container.brick_detail(brick)
+                spent += size
+                self.fetched_bytes_total += size
+                adjusted.append((brick, 0))
+            else:
+                deferred += 1
+                self.fallback_log.append((self._frame, brick))
+                if self.container.meta.brick_log2 >= 2:
+                    adjusted.append((brick, 1))
+        self.deferred_last_frame = deferred
+        self._frame += 1
+        return adjusted
+
+    def take(self, brick: int):
+        """Hand the fetched stream to the decoder; it is not kept afterwards."""
+        return self.hot.pop(brick, None)
+
+
+class DeviceDetailStream(DetailStore):
+    """DetailStore whose streams reach the GPU decoder through one staged H2D copy per frame."""
+
+    def __init__(self, container, volume, budget_bytes: int = 8 << 20):
+        super().__init__(container, budget_bytes)
+        self.volume = volume
+        torch = volume._torch
+        self._torch = torch
+        self._cap = 0
+        self._host = None
+        self._dev = None
+        self.staged_bytes_total = 0
+        self.staged_last_frame = 0
+        self._ev = None
+
+    def _ensure(self, nbytes: int):
+        torch = self._torch
+        if nbytes > self._cap:
+            cap = max(nbytes, 1 << 16)
+            self._host = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            self._dev = torch.empty(cap + 64, dtype=torch.uint8, device=self.volume.device)
+            self._cap = cap
+
+    def stage(self, bricks, stream=None) -> None:
+        """Make the level-0 streams of `bricks` readable by the next decode (take semantics)."""
+        from .device import _ptr, _stream_handle
+        torch = self._torch
+        if self._ev is not None:
+            self._ev.synchronize()              # the previous frame's copy has left the pinned buffer
+        bricks = [int(b) for b in bricks]
+        streams = []
+        for b in bricks:
+            s = self.take(b)
+            if s is None:                       # not fetched this frame: read it now (render.py:876-878)
+                s = self.container.brick_detail(b)
+            streams.append(np.asarray(s, dtype=np.uint8))
+        lens = np.array([s.size for s in streams], dtype=np.int64)
+        offs = np.zeros(len(streams), dtype=np.int64)
+        if len(streams) > 1:
+            offs[1:] = np.cumsum(lens)[:-1]
+        total = int(lens.sum())
+        self._ensure(max(total, 1))
+        host = self._host.numpy()
+        for o, s in zip(offs, streams):
+            host[o: o + s.size] = s
+        dev = self.volume.device
+        with torch.cuda.device(dev):
+            if total:
+                self._dev[:total].copy_(self._host[:total], non_blocking=True)
+                self._ev = torch.cuda.Event()
+                self._ev.record()
+            b_t = torch.as_tensor(np.asarray(bricks, dtype=np.int64)).to(dev, torch.int32)
+            o_t = torch.as_tensor(offs).to(dev)
+            l_t = torch.as_tensor(lens).to(dev, torch.int32)
+            _lib.check(_lib.lib().csv_volume_stage_detail(
+                self.volume._h, _ptr(b_t) if bricks else 0, _ptr(o_t) if bricks else 0, _ptr(l_t) if bricks else 0,
+                len(bricks), _ptr(self._dev), total, _stream_handle(torch, stream)))
+        self.staged_bytes_total += total
+        self.staged_last_frame = total
