@@ -476,13 +476,21 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
     unsigned long long ek = ~0ull;
     if ((uint64_t)e0 + 8ull * nact > nvalid) ek = ekey(nvalid, 0, EK_UNDERRUN_NV);
     // palette base per active parent, in entry (rank) order (codec.py:453-457) -> per-warp scratch
-    for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
-        const uint32_t k = k0 + lane;
-        const uint32_t ent0 = e0 + 8 * k;
-        const uint64_t w = (k < nact && ent0 + 8 <= cap) ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
-        const uint32_t c6 = __popcll(m_op6(w)), inc6 = warp_incl(c6, lane);
-        if (k < nact) B.ipb[k] = (uint16_t)(ip_run + inc6 - c6);
-        ip_run += __shfl_sync(FULL, inc6, 31);
+    {
+        auto ld = [&](uint32_t k) -> uint64_t {
+            const uint32_t ent0 = e0 + 8 * k;
+            return (k < nact && ent0 + 8 <= cap) ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+        };
+        uint64_t wn = ld(lane), wnn = ld(32 + lane);   // two chunks in flight
+        for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const uint64_t w = wn;
+            wn = wnn;
+            wnn = ld(k0 + 64 + lane);
+            const uint32_t c6 = __popcll(m_op6(w)), inc6 = warp_incl(c6, lane);
+            if (k < nact) B.ipb[k] = (uint16_t)(ip_run + inc6 - c6);
+            ip_run += __shfl_sync(FULL, inc6, 31);
+        }
     }
     __syncwarp();
     using P2 = typename IX<IT>::P2;
@@ -577,6 +585,7 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
                 for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
                     const uint32_t k = k0 + lane;
                     uint32_t m = k < nl ? (uint32_t)pdesc[k] & cls : 0u;
+                    if (!__any_sync(FULL, m != 0u)) continue;
                     const uint32_t i = m ? plist[k] : 0u;
                     const uint32_t cx0 = 2 * (i % RR), cy0 = 2 * (i / RR);
                     while (m) {
