@@ -180,3 +180,65 @@ def test_stats_errors_match_rans_decode(pkg):
     c.directory = d
     with pytest.raises(pkg.CorruptStreamError, match="entropy stream (truncated at symbol|desynchronized)"):
         pkg.stats(c)
+
+
+def test_mixed_palette_widths(pkg, oracle):
+    """One volume whose bricks need both K2w passes (u8 indices for palettes <= 256
+    entries, u16 above; both run in the same decode): raster at every LOD and a
+    mixed-LOD Morton batch, bit-exact against the oracle."""
+    import torch
+    rng = np.random.default_rng(11)
+    b = 32
+    vol = np.zeros((2 * b, 2 * b, 3 * b), dtype=np.uint32)          # (Z, Y, X): 12 bricks
+    zz, yy, xx = np.meshgrid(np.arange(2 * b), np.arange(2 * b), np.arange(3 * b), indexing="ij")
+    vol[:] = (xx // 9 + 7 * (yy // 11) + 31 * (zz // 13)).astype(np.uint32)   # smooth: small palettes
+    for (bz, by, bx) in [(0, 0, 0), (1, 1, 2), (0, 1, 1), (1, 0, 1)]:      # noise bricks: ~32k labels
+        vol[bz * b:(bz + 1) * b, by * b:(by + 1) * b, bx * b:(bx + 1) * b] = rng.integers(
+            0, 1 << 31, size=(b, b, b), dtype=np.uint32)
+    vol[b:, b:, :b][::2, ::3, ::5] = 5                                    # a brick with ~300 labels
+    vol[b:, b:, :b][1::2] = rng.integers(0, 300, size=vol[b:, b:, :b][1::2].shape, dtype=np.uint32)
+    oc = oracle.compress_volume(vol, brick_log2=5)
+    pal = oc.directory[:, 1]
+    assert pal.max() > 256 and pal.min() <= 256
+    c = pkg.CsvContainer.from_bytes(oc.to_bytes())
+    for t in range(6):
+        bad, _, ref = oracle.decompress_volume(oc, t)
+        assert bad == -1
+        assert np.array_equal(pkg.decompress_volume(c, t), ref), t
+    v = c.to_device()
+    n = oc.n_bricks
+    reqs = [(i, t) for i in range(n) for t in (0, 1, 2)]
+    sizes = [8 ** (5 - t) for _, t in reqs]
+    dst = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    pool = torch.zeros(int(sum(sizes)), dtype=torch.int32, device="cuda")
+    res = v.decode_bricks(torch.tensor([r[0] for r in reqs], dtype=torch.int32, device="cuda"),
+                          torch.tensor([r[1] for r in reqs], dtype=torch.uint8, device="cuda"),
+                          torch.from_numpy(dst).cuda(), pool)
+    pkg.GpuVolume.raise_first(res, len(reqs))
+    host = pool.cpu().numpy().view(np.uint32)
+    for k, (i, t) in enumerate(reqs):
+        _, ref = oracle.container_decode_brick(oc, i, t)
+        assert np.array_equal(host[dst[k]: dst[k] + sizes[k]], ref), (i, t)
+
+
+def test_cta_fallback_kernel(tmp_path):
+    """The CTA-per-brick replay (k2_fast) still serves palettes > 65535 entries; force it
+    for a whole process (CSVGPU_K2=cta) and check goldens at every LOD, raster and Morton."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, json, hashlib, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2308_16619_b200 as p
+from conftest import golden_bytes, golden_json, h16
+for name in ["a_b3", "d_b5_mem", "h_b3_u16", "f_b2_noise"]:
+    g = golden_json("decode_%%s.json" %% name)
+    c = p.CsvContainer.from_bytes(golden_bytes(name))
+    for t in range(g["brick_log2"] + 1):
+        assert h16(p.decompress_volume(c, t)) == g["volume"][str(t)], (name, t)
+print("cta ok")
+""" % (os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."),)
+    env = dict(os.environ, CSVGPU_K2="cta", PYTHONPATH=os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "cta ok" in r.stdout, r.stderr[-2000:]
