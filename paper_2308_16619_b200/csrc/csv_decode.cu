@@ -273,12 +273,15 @@ __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t ite
     return true;
 }
 
-// One symbol; returns false when the lane's item is finished.
-template <bool ENTROPY, bool COUNT>
+// One symbol; returns false when the lane's item is finished.  With REFILL =
+// false the caller guarantees >= 16 buffered bits (pairs of steps after one
+// `nb < 32` refill: the refill block then runs on every other step of the warp
+// instead of nearly every step, since some lane always needs bytes).
+template <bool ENTROPY, bool COUNT, bool REFILL = true>
 __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t* tab) {
     uint32_t s;
     if (ENTROPY) {
-        if (L.nb < 16) lane_refill(L);
+        if (REFILL && L.nb < 16) lane_refill(L);
         uint32_t e = tab[(L.tsel << 12) | (L.x & (kTotalFreq - 1))];
         s = e & 15u;
         uint32_t xn = (e >> 16) * (L.x >> kPrecision) + ((e >> 4) & 0xFFFu);
@@ -308,6 +311,7 @@ __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t
                 ++L.pos;
             }
             L.x = xn;
+            if (!REFILL && L.nb < 16) lane_refill(L);   // the pair's next step reads without a check
         }
     } else {
         s = (L.rawp[L.i >> 1] >> (4 * (L.i & 1))) & 15u;
@@ -351,9 +355,18 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MINB) k1_streams(VolView V, Pla
         }
         if (__all_sync(FULL, done)) break;
         if (has) {
+            if (ENTROPY) {
+#pragma unroll 2
+                for (int u = 0; u < 16; ++u) {
+                    if (L.nb < 32) lane_refill(L);
+                    if (!lane_step<ENTROPY, COUNT, false>(L, P, tab)) { has = false; break; }
+                    if (!lane_step<ENTROPY, COUNT, false>(L, P, tab)) { has = false; break; }
+                }
+            } else {
 #pragma unroll 4
-            for (int u = 0; u < 32; ++u) {
-                if (!lane_step<ENTROPY, COUNT>(L, P, tab)) { has = false; break; }
+                for (int u = 0; u < 32; ++u) {
+                    if (!lane_step<ENTROPY, COUNT>(L, P, tab)) { has = false; break; }
+                }
             }
             if (COUNT && has && L.since > 16000u) lane_flush_counts(L, P.op_counts);
         }
