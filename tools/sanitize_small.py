@@ -1,6 +1,8 @@
 """Small decode workload for compute-sanitizer runs (memcheck / racecheck / synccheck):
-config-1 container at LOD 0 and 2 (raster), a batched Morton decode with mixed LODs,
-a b=64 container (global-workspace kernel) and stats() (K1 count mode)."""
+config-1 container at LOD 0 and 2 (raster, K2w u8 pass), a batched Morton decode with
+mixed LODs, a b=64 container (global-workspace kernel), stats() (K1 count mode), a
+noise container whose palettes need the u16 K2w pass, and one device-cache frame with
+LOD selection, visibility and cold-detail staging."""
 import os
 import sys
 
@@ -27,5 +29,26 @@ with open(os.path.join(G, "vol_g_b6.csv1"), "rb") as f:
     g = p.CsvContainer.from_bytes(f.read())
 p.decompress_volume(g, 0)
 s = p.stats(p.CsvContainer.from_bytes(open(os.path.join(G, "vol_d_b5_mem.csv1"), "rb").read()))
+k = p.CsvContainer.from_bytes(open(os.path.join(G, "vol_k_b5_noise_raw.csv1"), "rb").read())
+p.decompress_volume(k, 0)
+# device frame: LODs, visibility, cache assign, cold detail
+import tempfile
+with tempfile.TemporaryDirectory() as td:
+    path = os.path.join(td, "d.csv1")
+    open(path, "wb").write(open(os.path.join(G, "vol_d_b5_mem.csv1"), "rb").read())
+    cold = p.CsvContainer.open(path, detail_cold=True)
+    cv = cold.to_device()
+    lods = p.desired_lods_device(cv, p.Camera(position=(0.0, 0.0, 0.0), height=64))
+    vis = p.visibility_mask_device(cv, p.TransferFunction(0.0, {0: (1.0, 1.0, 1.0, 1.0)}))
+    nb = cold.meta.brick_count
+    cache = p.DeviceBrickCache(nb, 5, pool_bytes=nb * 8 ** 4 * 32 + 4096)
+    ds = p.DeviceDetailStream(cold, cv, budget_bytes=4096)
+    cache.begin_frame()
+    req = [(i, 0) for i in range(nb)]
+    cache.mark_used([r[0] for r in req], [0] * nb)
+    adj = ds.plan(req)
+    cache.end_frame_assign([a[0] for a in adj], [a[1] for a in adj], cv, detail=ds)
+    cache.close()
+    cv.close()
 torch.cuda.synchronize()
 print("sanitize workload ok", s["total_ops"])
