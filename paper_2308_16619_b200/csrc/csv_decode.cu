@@ -138,7 +138,7 @@ struct Lane {
     int nb;                 // valid bits in buf
     int cw;                 // words left in cq
     int k;                  // entries in acc
-    int tsel;               // decode table (0 interior, 1 leaf)
+    uint32_t tbase;         // decode table offset in shared memory (0 interior, 4096 leaf)
     uint32_t since;         // count mode: ops since the last flush
     bool pend;              // next nibble is a P_delta payload
     bool slow;              // first step from a state < 2^23 (corrupt streams only)
@@ -236,7 +236,7 @@ __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t ite
     bool ok = b < V.nb && t < V.N && !(s == 1 && t != 0);
     L.n = ok ? eff_nibbles(V, b, s) : 0;
     L.lim = ok ? (COUNT ? L.n : stream_limit(V, b, t, s)) : 0;
-    L.tsel = s;
+    L.tbase = (uint32_t)s << 12;
     if (!ok) {
         L.n = 0; L.lim = 0;
         P.sres[w] = csv_stream_result{0, 0xffffffffu, 0, 0};
@@ -277,15 +277,17 @@ __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t ite
 // false the caller guarantees >= 16 buffered bits (pairs of steps after one
 // `nb < 32` refill: the refill block then runs on every other step of the warp
 // instead of nearly every step, since some lane always needs bytes).
-template <bool ENTROPY, bool COUNT, bool REFILL = true>
+// SLOWCHK = false: the caller has already taken the (rare) first step of a
+// stream whose initial state is below 2^23, so no per-step check is needed.
+template <bool ENTROPY, bool COUNT, bool REFILL = true, bool SLOWCHK = true>
 __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t* tab) {
     uint32_t s;
     if (ENTROPY) {
         if (REFILL && L.nb < 16) lane_refill(L);
-        uint32_t e = tab[(L.tsel << 12) | (L.x & (kTotalFreq - 1))];
+        uint32_t e = tab[L.tbase + (L.x & (kTotalFreq - 1))];
         s = e & 15u;
         uint32_t xn = (e >> 16) * (L.x >> kPrecision) + ((e >> 4) & 0xFFFu);
-        if (!L.slow) {
+        if (!SLOWCHK || !L.slow) {
             // after a step from x >= 2^23, x >= 2^11: at most two renorm bytes
             uint32_t r = (xn < kStateLower) + (xn < (1u << 15));
             if (L.pos + r > L.len) {           // underrun (codec.py:295-297)
@@ -356,11 +358,14 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MINB) k1_streams(VolView V, Pla
         if (__all_sync(FULL, done)) break;
         if (has) {
             if (ENTROPY) {
+                if (L.slow && !lane_step<ENTROPY, COUNT, true, true>(L, P, tab)) has = false;
+                if (has) {
 #pragma unroll 2
-                for (int u = 0; u < 16; ++u) {
-                    if (L.nb < 32) lane_refill(L);
-                    if (!lane_step<ENTROPY, COUNT, false>(L, P, tab)) { has = false; break; }
-                    if (!lane_step<ENTROPY, COUNT, false>(L, P, tab)) { has = false; break; }
+                    for (int u = 0; u < 16; ++u) {
+                        if (L.nb < 32) lane_refill(L);
+                        if (!lane_step<ENTROPY, COUNT, false, false>(L, P, tab)) { has = false; break; }
+                        if (!lane_step<ENTROPY, COUNT, false, false>(L, P, tab)) { has = false; break; }
+                    }
                 }
             } else {
 #pragma unroll 4
