@@ -11,14 +11,15 @@
 //                     operation and stores them 8 at a time.  Lanes refill
 //                     work dynamically from a global counter (warp-aggregated
 //                     atomics), detail streams (long) first.
-//  K2 k2_replay    -- replay stage.  One CTA per brick, level-synchronous:
-//                     per level a popcount rank of active parents locates each
-//                     parent's 8 entries, a block scan of palette-advance
-//                     counts gives i_p, every child is evaluated independently
-//                     (same-level neighbour chains resolved directly, <=3
-//                     hops), and the final level streams straight to HBM in
-//                     raster (K3, decompress_volume) or Morton pool order (K4,
-//                     brick cache).
+//  K2w k2_warp     -- replay stage (csv_replay_warp.cuh), the default: one
+//                     WARP per brick, persistent warps, values as u8/u16
+//                     palette indices, compacted active parents, chain rounds
+//                     by popcount class, plane-sweep final level written to HBM
+//                     as whole raster rows (K3, decompress_volume) or Morton
+//                     sectors (K4, brick cache).
+//  K2 k2_fast / k2_replay -- the earlier CTA-per-brick level-synchronous replay
+//                     (csv_replay_fast.cuh, below): kept for palettes > 65535
+//                     entries and for N - t = 6, 7 (global workspace).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
