@@ -655,10 +655,10 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
 }  // namespace wk
 
 #ifndef K2W_MINB
-#define K2W_MINB 10
+#define K2W_MINB 20
 #endif
 #ifndef K2W_WPB
-#define K2W_WPB 2
+#define K2W_WPB 1
 #endif
 constexpr int K2W_WARPS = K2W_WPB;
 
