@@ -329,7 +329,7 @@ __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t
 
 template <bool ENTROPY, bool COUNT>
 #ifndef K1_MINB
-#define K1_MINB 4
+#define K1_MINB 3
 #endif
 __global__ void __launch_bounds__(K1_THREADS, K1_MINB) k1_streams(VolView V, Plan P, unsigned long long* counter) {
     __shared__ uint32_t tab[2 * 4096];
