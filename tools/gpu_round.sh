@@ -8,3 +8,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k1_streams|k2_warp" -c 2 -o gpurun_out/prof_full python bench.py --profile --steps 1 --warmup 1 --no-cache > gpurun_out/ncu.log 2>&1
 tail -3 gpurun_out/ncu.log
 cat gpurun_out/pytest_gpu.txt gpurun_out/smoke.txt gpurun_out/bench.json
+timeout 600 python bench.py --workload config2 --no-e2e --no-cpu --no-cache > gpurun_out/bench_config2.json 2>/dev/null
+tail -1 gpurun_out/bench_config2.json
