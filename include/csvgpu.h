@@ -125,6 +125,10 @@ int csv_volume_stage_detail(csv_volume* vol, const uint32_t* d_bricks, const uin
 
 int csv_volume_free(csv_volume* vol);
 
+/* DetailStore.plan's budget scan (render.py:808-823), host-side C: accept[i] = 1 iff
+ * the running total of accepted sizes plus sizes[i] stays within budget. */
+int csv_detail_plan_greedy(const uint64_t* sizes, uint64_t n, uint64_t budget, uint8_t* accept, uint64_t* spent);
+
 /* Full-volume decode at LOD t into a raster (Z,Y,X) u32 slab: replaces
  * decompress_volume (container.py:456-478) + morton_to_grid (morton.py:411-416).
  * d_out holds LOD-t z rows [z_begin, z_end) of the volume cropped to

@@ -28,7 +28,7 @@ EXPORTS = (
     "csv_desired_lods", "csv_visibility_mask", "csv_cache_create", "csv_cache_free", "csv_cache_begin_frame",
     "csv_cache_mark_used", "csv_cache_assign", "csv_cache_state", "csv_cache_counters", "csv_cache_stack_heights",
     "csv_cache_read_state", "csv_cache_plan", "csv_cache_decode_fills", "csv_volume_stage_detail",
-    "csv_cache_read_fills",
+    "csv_cache_read_fills", "csv_detail_plan_greedy",
 )
 
 
@@ -118,6 +118,8 @@ def lib():
         L.csv_volume_stage_detail.argtypes = [P, P, P, P, U64, P, U64, UP]
         L.csv_cache_read_fills.restype = I
         L.csv_cache_read_fills.argtypes = [P, P, P, U64, P]
+        L.csv_detail_plan_greedy.restype = I
+        L.csv_detail_plan_greedy.argtypes = [P, U64, U64, P, P]
         L.csv_cache_read_state.restype = I
         L.csv_cache_read_state.argtypes = [P, P, P]
         L.csv_cache_counters.restype = I

@@ -400,6 +400,21 @@ int csv_volume_stage_detail(csv_volume* vol, const uint32_t* d_bricks, const uin
     return CSV_OK;
 }
 
+// DetailStore.plan's budget scan (render.py:808-823), host-side: candidates in
+// request order are fetched while the running total stays within the budget;
+// a candidate that does not fit is deferred and the scan continues.
+int csv_detail_plan_greedy(const uint64_t* sizes, uint64_t n, uint64_t budget, uint8_t* accept, uint64_t* spent) {
+    if ((n && (!sizes || !accept)) || !spent) return fail(CSV_E_ARG, "null argument");
+    uint64_t sp = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const bool ok = sp + sizes[i] <= budget;
+        accept[i] = ok ? 1 : 0;
+        if (ok) sp += sizes[i];
+    }
+    *spent = sp;
+    return CSV_OK;
+}
+
 int csv_volume_free(csv_volume* vol) {
     vol_release(vol);
     return CSV_OK;

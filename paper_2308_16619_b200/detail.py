@@ -37,6 +37,9 @@ class DetailStore:
 
     def plan(self, requests) -> list[tuple[int, int]]:
         """Fetch detail for level-0 requests within budget; downgrade the rest to level 1."""
+        if len(requests) > 256:             # same result, vectorised (numpy + the C budget scan)
+            b, l = self.plan_arrays(requests)
+            return list(zip(b.tolist(), l.tolist()))
         spent = 0
         deferred = 0
         adjusted: list[tuple[int, int]] = []
@@ -61,6 +64,36 @@ class DetailStore:
         self.deferred_last_frame = deferred
         self._frame += 1
         return adjusted
+
+    def plan_arrays(self, requests):
+        """plan() with numpy: (bricks int64, lods int64) of the adjusted, sorted, unique requests."""
+        r = np.asarray(requests, dtype=np.int64).reshape(-1, 2)
+        key = np.unique(r[:, 0] * 256 + r[:, 1])                  # sorted(set(requests))
+        bricks, lods = key >> 8, key & 255
+        lod0 = lods == 0
+        sizes = self.container.directory["detail_bytes"].astype(np.int64)[bricks]
+        hot = np.fromiter(self.hot.keys(), dtype=np.int64, count=len(self.hot))
+        cand = lod0 & (sizes > 0) & ~np.isin(bricks, hot)
+        cs = np.ascontiguousarray(sizes[cand], dtype=np.uint64)
+        acc = np.zeros(cs.size, dtype=np.uint8)
+        spent = ctypes.c_uint64()
+        _lib.check(_lib.lib().csv_detail_plan_greedy(cs.ctypes.data, cs.size, int(self.budget_bytes),
+                                                     acc.ctypes.data, ctypes.byref(spent)))
+        ci = np.flatnonzero(cand)
+        fetched, deferred = ci[acc == 1], ci[acc == 0]
+        for b in bricks[fetched].tolist():
+            self.hot[b] = self.container.brick_detail(b)
+        self.fetched_bytes_total += int(sizes[fetched].sum())
+        self.deferred_last_frame = int(deferred.size)
+        self.fallback_log.extend((self._frame, b) for b in bricks[deferred].tolist())
+        self._frame += 1
+        keep = np.ones(bricks.size, dtype=bool)
+        out_l = lods.copy()
+        if self.container.meta.brick_log2 >= 2:
+            out_l[deferred] = 1
+        else:
+            keep[deferred] = False
+        return bricks[keep], out_l[keep]
 
     def take(self, brick: int):
         """Hand the fetched stream to the decoder; it is not kept afterwards."""
@@ -110,8 +143,8 @@ class DeviceDetailStream(DetailStore):
         total = int(lens.sum())
         self._ensure(max(total, 1))
         host = self._host.numpy()
-        for o, s in zip(offs, streams):
-            host[o: o + s.size] = s
+        if total:
+            np.concatenate(streams, out=host[:total])
         dev = self.volume.device
         with torch.cuda.device(dev):
             if total:
