@@ -81,8 +81,16 @@ class DetailStore:
                                                      acc.ctypes.data, ctypes.byref(spent)))
         ci = np.flatnonzero(cand)
         fetched, deferred = ci[acc == 1], ci[acc == 0]
-        for b in bricks[fetched].tolist():
-            self.hot[b] = self.container.brick_detail(b)
+        fb = bricks[fetched]
+        blob = getattr(self.container, "detail_blob", None)
+        if blob is not None and fb.size:         # in-memory detail: slice views in one pass
+            d = self.container.directory
+            offs = d["detail_off"].astype(np.int64)[fb].tolist()
+            lens = d["detail_bytes"].astype(np.int64)[fb].tolist()
+            self.hot.update({b: blob[o: o + n] for b, o, n in zip(fb.tolist(), offs, lens)})
+        else:
+            for b in fb.tolist():
+                self.hot[b] = self.container.brick_detail(b)
         self.fetched_bytes_total += int(sizes[fetched].sum())
         self.deferred_last_frame = int(deferred.size)
         self.fallback_log.extend((self._frame, b) for b in bricks[deferred].tolist())
