@@ -16,6 +16,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CSVGPU_LIB") or os.path.join(_PKG, "libcsvgpu.so")   # override: build variants
 _lib = None
 
+# C-ABI return codes (include/csvgpu.h)
+CSV_E_ARG, CSV_E_CUDA, CSV_E_NOMEM, CSV_E_FORMAT, CSV_E_CAPACITY = -1, -2, -3, -4, -5
+
 RESULT_DTYPE = np.dtype([("status", "<i4"), ("stream", "<i4"), ("pos", "<i8"), ("ci", "<i8"), ("di", "<i8")])
 STREAM_RESULT_DTYPE = np.dtype([("n_entries", "<u4"), ("fail_nibble", "<u4"), ("flags", "<u4"), ("partial_op", "<u4")])
 
