@@ -221,7 +221,8 @@ def desired_lods(grid, b, cam, fov, height, max_lod):
 def timeseries_leg(p, torch, dev, stream, steps: int = 2, dims=(1024, 1024, 1024), cells: int = 22):
     """1024^3 Voronoi timesteps (seed 3, seeds drifting
     by <= k voxels at step k); per timestep GPU encode then GPU decode, both
-    timed with CUDA events; lossless round trip checked (untimed)."""
+    timed with CUDA events (the decode after one untimed call that allocates the
+    new volume's workspace); lossless round trip checked (untimed)."""
     enc_ms, dec_ms = [], []
     X, Y, Z = dims
     for k in range(steps):
@@ -234,6 +235,7 @@ def timeseries_leg(p, torch, dev, stream, steps: int = 2, dims=(1024, 1024, 1024
         e1.record(stream)
         gv = enc.to_volume()
         out = torch.empty_like(vol)
+        gv.decode(0, out=out)               # untimed: sizes this volume's decode workspace (one-off cudaMalloc)
         torch.cuda.synchronize()
         e1b = torch.cuda.Event(enable_timing=True)
         e1b.record(stream)
