@@ -126,19 +126,18 @@ struct Lane {
     uint4 cq;               // current chunk (words consumed from .x, rotated)
     uint4 nq;               // prefetched chunk
     uint64_t buf;           // upcoming stream bits, MSB first
-    uint64_t acc;           // entry bytes of the group being built (<= 8)
+    uint32_t alo, ahi;      // last <= 8 entry bytes, newest in the top byte of ahi
     uint64_t* outp;         // entry region (32-byte aligned)
     uint64_t c03, c47;      // count mode: per-op counters, 4 x 16 bits each
     const uint8_t* rawp;    // raw mode: packed nibble bytes
     uint32_t x;             // rANS state (fits 32 bits: f*(x>>12) < 2^32)
     uint32_t pos, len;      // bytes consumed (incl. 4 state bytes) / stream bytes
     uint32_t i, lim, n;     // nibble index, nibble limit, stored count
-    uint32_t g4;            // 8-entry groups stored
+    uint32_t ne;            // entries emitted
     uint32_t cur;           // current entry byte
     uint64_t item;
     int nb;                 // valid bits in buf
     int cw;                 // words left in cq
-    int k;                  // entries in acc
     uint32_t tbase;         // decode table offset in shared memory (0 interior, 4096 leaf)
     uint32_t since;         // count mode: ops since the last flush
     bool pend;              // next nibble is a P_delta payload
@@ -189,20 +188,22 @@ __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
     }
     L.cur = pay ? (L.cur | (s << 4)) : s;
     if (!L.pend) {
-        L.acc |= (uint64_t)L.cur << (8 * L.k);
-        if (++L.k == 8) {
-            L.outp[L.g4++] = L.acc;
-            L.acc = 0;
-            L.k = 0;
-        }
+        // shift the 8-byte window down one byte and append the entry on top: after
+        // 8 appends the first entry sits in the lowest byte (little-endian order)
+        L.alo = __byte_perm(L.alo, L.ahi, 0x4321);
+        L.ahi = __byte_perm(L.ahi, L.cur, 0x4321);
+        if ((++L.ne & 7u) == 0u) L.outp[(L.ne >> 3) - 1] = ((uint64_t)L.ahi << 32) | L.alo;
     }
 }
 
 __device__ __forceinline__ void lane_finish(Lane& L, const Plan& P, bool failed, bool entropy) {
     if (P.op_counts) lane_flush_counts(L, P.op_counts);
-    else if (L.k > 0) L.outp[L.g4] = L.acc;
+    else if (L.ne & 7u) {   // partial group: move its entries down to byte 0, zero above
+        const uint64_t a = ((uint64_t)L.ahi << 32) | L.alo;
+        L.outp[L.ne >> 3] = a >> (8 * (8 - (L.ne & 7u)));
+    }
     csv_stream_result r;
-    r.n_entries = L.g4 * 8 + L.k;
+    r.n_entries = L.ne;
     r.flags = 0;
     r.fail_nibble = 0xffffffffu;
     r.partial_op = 0;
@@ -228,7 +229,7 @@ __device__ bool lane_init(Lane& L, const VolView& V, const Plan& P, uint64_t ite
     int s = item < P.n ? 1 : 0;           // detail streams first (longest chains)
     uint64_t w = 2 * r + s;               // result / region index
     L.item = w;
-    L.acc = 0; L.k = 0; L.g4 = 0; L.pend = false; L.cur = 0; L.i = 0; L.slow = false;
+    L.alo = 0; L.ahi = 0; L.ne = 0; L.pend = false; L.cur = 0; L.i = 0; L.slow = false;
     L.x = 0; L.pos = 0; L.len = 0; L.nb = 0; L.buf = 0;
     uint64_t b = req_local(V, P, r);
     int t = req_lod(P, r);

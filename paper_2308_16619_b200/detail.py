@@ -154,7 +154,9 @@ class DeviceDetailStream(DetailStore):
         if total:
             np.concatenate(streams, out=host[:total])
         dev = self.volume.device
-        with torch.cuda.device(dev):
+        with torch.cuda.device(dev), torch.cuda.stream(stream if stream is not None
+                                                      else torch.cuda.current_stream()):
+            # copy, index uploads, event and staging kernel all on the caller's stream
             if total:
                 self._dev[:total].copy_(self._host[:total], non_blocking=True)
                 self._ev = torch.cuda.Event()
