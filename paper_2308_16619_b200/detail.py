@@ -17,10 +17,53 @@ itself never holds the detail blob.
 from __future__ import annotations
 
 import ctypes
+from collections.abc import Sequence
 
 import numpy as np
 
 from . import _lib
+
+
+class FallbackLog(Sequence):
+    """The (frame, brick) fallback list of DetailStore, kept as one brick array per
+    frame so a 40k-brick frame costs one array copy; it reads like the reference's
+    list of tuples (len, indexing, iteration, ==)."""
+
+    def __init__(self):
+        self._chunks: list[tuple[int, np.ndarray]] = []
+        self._n = 0
+        self._flat = None
+
+    def append(self, item) -> None:
+        self._chunks.append((int(item[0]), np.array([item[1]], dtype=np.int64)))
+        self._n += 1
+        self._flat = None
+
+    def extend_frame(self, frame: int, bricks: np.ndarray) -> None:
+        if bricks.size:
+            self._chunks.append((int(frame), np.array(bricks, dtype=np.int64)))
+            self._n += int(bricks.size)
+            self._flat = None
+
+    def clear(self) -> None:
+        self._chunks, self._n, self._flat = [], 0, None
+
+    def _list(self) -> list:
+        if self._flat is None:
+            self._flat = [(f, b) for f, a in self._chunks for b in a.tolist()]
+        return self._flat
+
+    def __len__(self) -> int:
+        return self._n
+
+    def __getitem__(self, i):
+        return self._list()[i]
+
+    def __eq__(self, other) -> bool:
+        return self._list() == list(other)
+
+    def __repr__(self) -> str:
+        return repr(self._list())
 
 
 class DetailStore:
@@ -32,7 +75,7 @@ class DetailStore:
         self.hot: dict[int, np.ndarray] = {}
         self.fetched_bytes_total = 0
         self.deferred_last_frame = 0
-        self.fallback_log: list[tuple[int, int]] = []  # (frame, brick)
+        self.fallback_log = FallbackLog()  # (frame, brick) pairs
         self._frame = 0
 
     def plan(self, requests) -> list[tuple[int, int]]:
@@ -68,10 +111,15 @@ class DetailStore:
     def plan_arrays(self, requests):
         """plan() with numpy: (bricks int64, lods int64) of the adjusted, sorted, unique requests."""
         r = np.asarray(requests, dtype=np.int64).reshape(-1, 2)
-        key = np.unique(r[:, 0] * 256 + r[:, 1])                  # sorted(set(requests))
+        key = np.sort(r[:, 0] * 256 + r[:, 1])                    # sorted(set(requests))
+        if key.size > 1:
+            key = key[np.concatenate(([True], key[1:] != key[:-1]))]
         bricks, lods = key >> 8, key & 255
         lod0 = lods == 0
-        sizes = self.container.directory["detail_bytes"].astype(np.int64)[bricks]
+        if getattr(self, "_dir64", None) is None:      # the directory is immutable: convert once
+            d = self.container.directory
+            self._dir64 = (d["detail_bytes"].astype(np.int64), d["detail_off"].astype(np.int64))
+        sizes = self._dir64[0][bricks]
         hot = np.fromiter(self.hot.keys(), dtype=np.int64, count=len(self.hot))
         cand = lod0 & (sizes > 0) & ~np.isin(bricks, hot)
         cs = np.ascontiguousarray(sizes[cand], dtype=np.uint64)
@@ -84,16 +132,15 @@ class DetailStore:
         fb = bricks[fetched]
         blob = getattr(self.container, "detail_blob", None)
         if blob is not None and fb.size:         # in-memory detail: slice views in one pass
-            d = self.container.directory
-            offs = d["detail_off"].astype(np.int64)[fb].tolist()
-            lens = d["detail_bytes"].astype(np.int64)[fb].tolist()
+            offs = self._dir64[1][fb].tolist()
+            lens = self._dir64[0][fb].tolist()
             self.hot.update({b: blob[o: o + n] for b, o, n in zip(fb.tolist(), offs, lens)})
         else:
             for b in fb.tolist():
                 self.hot[b] = self.container.brick_detail(b)
         self.fetched_bytes_total += int(sizes[fetched].sum())
         self.deferred_last_frame = int(deferred.size)
-        self.fallback_log.extend((self._frame, b) for b in bricks[deferred].tolist())
+        self.fallback_log.extend_frame(self._frame, bricks[deferred])
         self._frame += 1
         keep = np.ones(bricks.size, dtype=bool)
         out_l = lods.copy()
