@@ -299,18 +299,25 @@ def decompress_volume_device(container, t: int = 0, out=None, z_range=None, stre
     already resident in HBM.  With ``check`` the lowest failing brick raises
     the reference's CorruptStreamError.
     """
-    from .device import GpuVolume
+    from .device import GpuVolume, _on_stream
     vol = container if isinstance(container, GpuVolume) else container.to_device()
     if not 0 <= t <= vol.brick_log2:
         raise ValueError(f"LOD {t} outside [0, {vol.brick_log2}]")
     out, res = vol.decode(t, out=out, z_range=z_range, stream=stream)
     if check:
-        if t == vol.brick_log2:
-            n = vol.n_bricks
-            if n and bool((res[:n, 0] & 0xFFFFFFFF).eq(8).any()):
-                raise ValueError("expected 1 entries, got shape (0,)")   # morton_to_grid on palette[:1] of an empty palette
-        GpuVolume.raise_first(res, vol.n_bricks)
+        with _on_stream(vol._torch, vol.device, stream):   # read the results after the decode
+            _check_volume_results(vol, t, res)
     return out
+
+
+def _check_volume_results(vol, t, res):
+    """Raise the reference's exception for the lowest failing brick of a volume decode."""
+    from .device import GpuVolume
+    if t == vol.brick_log2:
+        n = vol.n_bricks
+        if n and bool((res[:n, 0] & 0xFFFFFFFF).eq(8).any()):
+            raise ValueError("expected 1 entries, got shape (0,)")   # morton_to_grid on palette[:1] of an empty palette
+    GpuVolume.raise_first(res, vol.n_bricks)
 
 
 def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None = None, out: np.ndarray | None = None,

@@ -51,6 +51,17 @@ def _stream_handle(torch, stream) -> int:
     return s.cuda_stream
 
 
+def _on_stream(torch, device, stream):
+    """Enter `device` and make `stream` torch's current stream, so that tensors allocated,
+    uploaded or read back around a C-ABI call are ordered with the kernels it launches."""
+    import contextlib
+    st = contextlib.ExitStack()
+    st.enter_context(torch.cuda.device(device))
+    if stream is not None:
+        st.enter_context(torch.cuda.stream(stream))
+    return st
+
+
 class GpuVolume:
     """One container (or a brick range of it) resident on a CUDA device.
 
@@ -130,6 +141,12 @@ class GpuVolume:
             _lib.lib().csv_volume_free(self._h)
             self._h = None
 
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
     def __del__(self):
         try:
             self.close()
@@ -161,11 +178,11 @@ class GpuVolume:
             raise ValueError(f"LOD {t} outside [0, {self.brick_log2}]")
         z0, z1 = z_range if z_range is not None else self.slab(t)
         _, cy, cx = self.crop(t)
-        if out is None:
-            out = torch.empty((max(z1 - z0, 0), cy, cx), dtype=torch.int32, device=self.device)
-        if results is None:
-            results = torch.empty((max(self.n_bricks, 1), 4), dtype=torch.int64, device=self.device)
-        with torch.cuda.device(self.device):
+        with _on_stream(torch, self.device, stream):
+            if out is None:
+                out = torch.empty((max(z1 - z0, 0), cy, cx), dtype=torch.int32, device=self.device)
+            if results is None:
+                results = torch.empty((max(self.n_bricks, 1), 4), dtype=torch.int64, device=self.device)
             _lib.check(_lib.lib().csv_decode_volume(self._h, t, _ptr(out), z0, z1, _ptr(results),
                                                     _stream_handle(torch, stream)))
         return out, results
@@ -180,7 +197,7 @@ class GpuVolume:
     def decode_range(self, t: int, brick_first: int, brick_last: int, out, z_range, results, stream=None):
         """Raster decode of bricks [brick_first, brick_last) into the z-slab `out` (rows z_range)."""
         torch = self._torch
-        with torch.cuda.device(self.device):
+        with _on_stream(torch, self.device, stream):
             _lib.check(_lib.lib().csv_decode_volume_range(self._h, t, brick_first, brick_last, _ptr(out),
                                                           z_range[0], z_range[1], _ptr(results),
                                                           _stream_handle(torch, stream)))
@@ -190,9 +207,9 @@ class GpuVolume:
         """Batched Morton decode (K1 + K2/K4) of (brick, lod) requests into pool[dst:...]."""
         torch = self._torch
         n = int(bricks.numel())
-        if results is None:
-            results = torch.empty((max(n, 1), 4), dtype=torch.int64, device=self.device)
-        with torch.cuda.device(self.device):
+        with _on_stream(torch, self.device, stream):
+            if results is None:
+                results = torch.empty((max(n, 1), 4), dtype=torch.int64, device=self.device)
             _lib.check(_lib.lib().csv_decode_bricks(self._h, n, _ptr(bricks), _ptr(lods), _ptr(dst), _ptr(pool),
                                                     _ptr(results), _stream_handle(torch, stream)))
         return results

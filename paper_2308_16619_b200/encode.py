@@ -43,6 +43,12 @@ class GpuEncoded:
             _lib.lib().csv_encoded_free(self._h)
             self._h = None
 
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
     def __del__(self):
         try:
             self.close()

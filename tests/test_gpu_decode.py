@@ -242,3 +242,31 @@ print("cta ok")
     env = dict(os.environ, CSVGPU_K2="cta", PYTHONPATH=os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "cta ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_side_stream_and_context_manager(pkg):
+    """Decodes issued on a non-default stream allocate, launch and check on that stream;
+    GpuVolume releases its device memory on leaving a `with` block."""
+    import torch
+    with open(GOLDEN + "/config1.csv1", "rb") as f:
+        c = pkg.CsvContainer.from_bytes(f.read())
+    ref = pkg.decompress_volume(c, 0)
+    side = torch.cuda.Stream()
+    with c.to_device() as vol:
+        for t in (0, 1):
+            out = pkg.decompress_volume_device(vol, t, stream=side)
+            side.synchronize()
+            assert np.array_equal(out.cpu().numpy().view(np.uint32), pkg.decompress_volume(c, t))
+        n = 64
+        bricks = torch.arange(n, dtype=torch.int32, device="cuda")
+        lods = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        dst = torch.arange(n, dtype=torch.int64, device="cuda") * 32 ** 3
+        pool = torch.empty(n * 32 ** 3, dtype=torch.int32, device="cuda")
+        res = vol.decode_bricks(bricks, lods, dst, pool, stream=side)
+        with torch.cuda.stream(side):
+            pkg.GpuVolume.raise_first(res, n)
+        side.synchronize()
+        pool2 = torch.empty_like(pool)
+        pkg.GpuVolume.raise_first(vol.decode_bricks(bricks, lods, dst, pool2), n)
+        assert torch.equal(pool, pool2) and ref.size > 0
+    assert vol._h is None
