@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <mutex>
 #include "csv_device.cuh"
 
 namespace csv {
@@ -553,15 +554,33 @@ void quantize(const unsigned long long* hist, uint16_t* out) {
 uint32_t max_ent_coarse(int N) { return max_entries(N, 0, 0); }
 uint32_t max_ent_detail(int N) { return max_entries(N, 0, 1); }
 
+// Per-device scratch arena, grow-only and reused by every encode on that device
+// (the encode synchronises its stream before returning, and the mutex serialises
+// encodes on one device).  Allocating the ~2 GB of chunk scratch per call made the
+// encode time depend on the driver's page-mapping cost (30 ms .. 1.4 s per 1024^3).
 struct Scratch {
     uint8_t* ent = nullptr; uint32_t* need = nullptr; uint32_t* pal = nullptr; uint32_t* cnt = nullptr;
     uint32_t* ws = nullptr; uint32_t* list = nullptr; uint64_t* sizes = nullptr; uint64_t* offs = nullptr;
     uint64_t* tmp = nullptr; unsigned long long* hist = nullptr;
-    void release() {
-        cudaFree(ent); cudaFree(need); cudaFree(pal); cudaFree(cnt); cudaFree(ws); cudaFree(list);
-        cudaFree(sizes); cudaFree(offs); cudaFree(tmp); cudaFree(hist);
-    }
+    uint64_t cap[10] = {};
 };
+struct ScratchArena {
+    std::mutex mu;
+    Scratch s;
+};
+constexpr int kMaxDevices = 64;
+ScratchArena g_arena[kMaxDevices];
+
+template <typename T>
+cudaError_t reserve(T** p, uint64_t* cap, uint64_t bytes) {
+    if (bytes <= *cap && *p) return cudaSuccess;
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes ? bytes : 16);
+    if (e == cudaSuccess) *cap = bytes;
+    return e;
+}
 
 }  // namespace
 
@@ -622,16 +641,17 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
     uint64_t per_brick = ent_stride + need_stride * 4 + pal_stride * 4 + 32 + (smem ? 0 : (uint64_t)Y_.words * 4);
     size_t freeb = 0, totb = 0;
     cudaMemGetInfo(&freeb, &totb);
-    uint64_t budget = std::min<uint64_t>((uint64_t)(freeb * 0.35), 6ull << 30);
+    uint64_t budget = std::min<uint64_t>((uint64_t)(freeb * 0.35), 2ull << 30);
     uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, budget / per_brick));
     chunk = std::min<uint64_t>(chunk, 65536);
 
-    Scratch Sc;
+    if (device < 0 || device >= kMaxDevices) return efail(CSV_E_ARG, "device index out of range");
+    std::lock_guard<std::mutex> arena_lock(g_arena[device].mu);
+    Scratch& Sc = g_arena[device].s;
     csv_encoded* enc = new csv_encoded();
     enc->device = device;
     enc->n = n;
     auto cleanup = [&](int rc, const char* msg) {
-        Sc.release();
         if (rc != CSV_OK) {
             cudaFree(enc->d_dir); cudaFree(enc->d_pal); cudaFree(enc->d_coarse); cudaFree(enc->d_detail);
             delete enc;
@@ -640,15 +660,15 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
         return CSV_OK;
     };
 #define ETRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return cleanup(CSV_E_CUDA, cudaGetErrorString(e_)); } while (0)
-    ETRY(cudaMalloc(&Sc.ent, chunk * ent_stride));
-    ETRY(cudaMalloc(&Sc.need, chunk * need_stride * 4));
-    ETRY(cudaMalloc(&Sc.pal, chunk * pal_stride * 4));
-    ETRY(cudaMalloc(&Sc.cnt, chunk * 32));
-    if (!smem) ETRY(cudaMalloc(&Sc.ws, chunk * (uint64_t)Y_.words * 4));
-    ETRY(cudaMalloc(&Sc.sizes, 3 * chunk * 8));
-    ETRY(cudaMalloc(&Sc.offs, (3 * chunk + 1) * 8));
-    ETRY(cudaMalloc(&Sc.tmp, 4104 * 8));
-    ETRY(cudaMalloc(&Sc.hist, 32 * 8));
+    ETRY(reserve(&Sc.ent, &Sc.cap[0], chunk * ent_stride));
+    ETRY(reserve(&Sc.need, &Sc.cap[1], chunk * need_stride * 4));
+    ETRY(reserve(&Sc.pal, &Sc.cap[2], chunk * pal_stride * 4));
+    ETRY(reserve(&Sc.cnt, &Sc.cap[3], chunk * 32));
+    if (!smem) ETRY(reserve(&Sc.ws, &Sc.cap[4], chunk * (uint64_t)Y_.words * 4));
+    ETRY(reserve(&Sc.sizes, &Sc.cap[5], 3 * chunk * 8));
+    ETRY(reserve(&Sc.offs, &Sc.cap[6], (3 * chunk + 1) * 8));
+    ETRY(reserve(&Sc.tmp, &Sc.cap[7], 4104 * 8));
+    ETRY(reserve(&Sc.hist, &Sc.cap[8], 32 * 8));
     ETRY(cudaMalloc(&enc->d_dir, n * 44 + 16));
     if (smem) ETRY(cudaFuncSetAttribute(e12_bricks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
 
@@ -667,7 +687,7 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
         uint64_t stride = prepass_stride < 1 ? 1 : (uint64_t)prepass_stride;
         std::vector<uint32_t> ids;
         for (uint64_t k = 0; k < n; k += stride) ids.push_back((uint32_t)k);
-        ETRY(cudaMalloc(&Sc.list, ids.size() * 4));
+        ETRY(reserve(&Sc.list, &Sc.cap[9], ids.size() * 4));
         ETRY(cudaMemcpyAsync(Sc.list, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, st));
         ETRY(cudaMemsetAsync(Sc.hist, 0, 32 * 8, st));
         for (uint64_t k0 = 0; k0 < ids.size(); k0 += chunk) {
@@ -715,6 +735,12 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
         ETRY(cudaStreamSynchronize(st));
         uint64_t tp = h[0], tc = h[1] - h[0], td = h[2] - h[1];
         // offsets of parts 1 and 2 are relative to the start of the whole scan: subtract in the kernel via bases
+        if (c0 == 0 && V.nb < n) {   // size the blobs once from the first chunk (+12.5 %), not by regrowth
+            const double sc = (double)n / (double)V.nb * 1.125;
+            ETRY(grow((void**)&enc->d_pal, &enc->cap[0], (uint64_t)(tp * 4 * sc) + kBlobPad, 0, st));
+            ETRY(grow((void**)&enc->d_coarse, &enc->cap[1], (uint64_t)(tc * sc) + kBlobPad, 0, st));
+            ETRY(grow((void**)&enc->d_detail, &enc->cap[2], (uint64_t)(td * sc) + kBlobPad, 0, st));
+        }
         ETRY(grow((void**)&enc->d_pal, &enc->cap[0], (pos[0] + tp) * 4 + kBlobPad, pos[0] * 4, st));
         ETRY(grow((void**)&enc->d_coarse, &enc->cap[1], pos[1] + tc + kBlobPad, pos[1], st));
         ETRY(grow((void**)&enc->d_detail, &enc->cap[2], pos[2] + td + kBlobPad, pos[2], st));
