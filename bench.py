@@ -342,7 +342,9 @@ def run_ours(args, world, rank, local):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom[0])
+            tj = json.load(f)
+        if tj.get("workload") == args.workload and not args.zlayers and (world == 1 or args.scaling == "weak"):
+            traffic = tj.get(dom[0])
     except Exception:
         pass
     achieved = dom[2] / (dom[1] * 1e-3) / 1e9

@@ -69,10 +69,12 @@ def main():
     with open(out_txt, "w") as f:
         f.write("\n".join(lines))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    tj = os.path.join(root, "profiles", "ncu_traffic.json")
-    with open(tj, "w") as f:
-        json.dump({"source": f"{os.path.relpath(out_txt, root)} (ncu --set full, one launch per kernel)", **traffic},
-                  f, indent=1)
+    if os.path.dirname(os.path.abspath(out_txt)) == os.path.join(root, "profiles"):
+        # only a summary committed under profiles/ feeds bench.py's roofline.traffic (config 3 captures)
+        tj = os.path.join(root, "profiles", "ncu_traffic.json")
+        with open(tj, "w") as f:
+            json.dump({"source": f"{os.path.relpath(out_txt, root)} (ncu --set full, one launch per kernel)",
+                       "workload": "config3", **traffic}, f, indent=1)
     print("\n".join(lines))
 
 
