@@ -199,7 +199,7 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
                       uintptr_t stream, csv_encoded** out);
 /* head120 = the CSV1 head; sizes3 = palette entries, coarse bytes, detail bytes. */
 int csv_encoded_info(csv_encoded* enc, uint8_t* head120, uint64_t* n_bricks, uint64_t* sizes3);
-/* Device pointers of the encoded directory rows and blobs (each padded by >= 16 B);
+/* Device pointers of the encoded directory rows and blobs (each with >= 64 readable bytes past its end);
  * valid until csv_encoded_free.  Suitable for csv_volume_create_device. */
 int csv_encoded_device_ptrs(csv_encoded* enc, const uint8_t** d_dir44, const uint32_t** d_palette,
                             const uint8_t** d_coarse, const uint8_t** d_detail);
