@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <mutex>
 #include "csv_device.cuh"
 
 namespace csv {
@@ -168,12 +169,45 @@ static int parse_head(const uint8_t* h, csv_volume* v, uint32_t* dtab_host) {
     return CSV_OK;
 }
 
+// Volume memory comes from the device's default stream-ordered pool, which keeps up
+// to kPoolKeep bytes of freed blocks mapped for the next volume: a host-in/host-out
+// decompress_volume creates and frees a ~2 GB volume per call, and plain
+// cudaMalloc/cudaFree of that made every call pay 10-850 ms of driver page mapping.
+// Frees follow a device synchronisation (the cudaFree semantics the callers rely on).
+constexpr uint64_t kPoolKeep = 8ull << 30;
+constexpr int kPoolDevices = 64;
+static std::once_flag g_pool_once[kPoolDevices];
+
+static void pool_init(int device) {
+    if (device < 0 || device >= kPoolDevices) return;
+    std::call_once(g_pool_once[device], [device] {
+        cudaMemPool_t mp;
+        if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
+            uint64_t keep = kPoolKeep;
+            cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t bytes, cudaStream_t st) {
+    return cudaMallocAsync(reinterpret_cast<void**>(p), bytes ? bytes : 16, st);
+}
+
+template <typename T>
+static void dfree(T*& p) {   // caller has synchronised the device (or the pointer's stream)
+    if (p) cudaFreeAsync(reinterpret_cast<void*>(p), 0);
+    p = nullptr;
+}
+
 static void vol_release(csv_volume* v) {
     if (!v) return;
     cudaSetDevice(v->device);
-    cudaFree(v->d_soa); cudaFree(v->d_blob); cudaFree(v->d_dtab);
-    cudaFree(v->d_sizes); cudaFree(v->d_eoff); cudaFree(v->d_scan); cudaFree(v->d_sres);
-    cudaFree(v->d_counter); cudaFree(v->d_entries); cudaFree(v->d_gws); cudaFree(v->d_wscratch);
+    cudaDeviceSynchronize();
+    dfree(v->d_soa); dfree(v->d_blob); dfree(v->d_dtab);
+    dfree(v->d_sizes); dfree(v->d_eoff); dfree(v->d_scan); dfree(v->d_sres);
+    dfree(v->d_counter); dfree(v->d_entries); dfree(v->d_gws); dfree(v->d_wscratch);
+    cudaStreamSynchronize(0);
     for (auto& e : v->ev) if (e) cudaEventDestroy(e);
     delete v;
 }
@@ -181,25 +215,25 @@ static void vol_release(csv_volume* v) {
 static int ensure_plan(csv_volume* v, uint64_t n, uint64_t entries_need, int Lg, cudaStream_t st) {
     if (n > v->plan_cap) {
         uint64_t cap = std::max<uint64_t>(n, 1024);
-        cudaFree(v->d_sizes); cudaFree(v->d_eoff); cudaFree(v->d_sres);
-        v->d_sizes = nullptr; v->d_eoff = nullptr; v->d_sres = nullptr; v->plan_cap = 0;
-        CUDA_TRY(cudaMalloc(&v->d_sizes, 2 * cap * sizeof(uint64_t)));
-        CUDA_TRY(cudaMalloc(&v->d_eoff, (2 * cap + 1) * sizeof(uint64_t)));
-        CUDA_TRY(cudaMalloc(&v->d_sres, 2 * cap * sizeof(csv_stream_result)));
+        if (v->d_sizes) CUDA_TRY(cudaDeviceSynchronize());
+        dfree(v->d_sizes); dfree(v->d_eoff); dfree(v->d_sres);
+        v->plan_cap = 0;
+        CUDA_TRY(dalloc(&v->d_sizes, 2 * cap * sizeof(uint64_t), st));
+        CUDA_TRY(dalloc(&v->d_eoff, (2 * cap + 1) * sizeof(uint64_t), st));
+        CUDA_TRY(dalloc(&v->d_sres, 2 * cap * sizeof(csv_stream_result), st));
         v->plan_cap = cap;
     }
-    if (!v->d_wscratch) CUDA_TRY(cudaMalloc(&v->d_wscratch, (size_t)v->nsm * 64 * kWScratchStride * sizeof(uint16_t)));
+    if (!v->d_wscratch) CUDA_TRY(dalloc(&v->d_wscratch, (size_t)v->nsm * 64 * kWScratchStride * sizeof(uint16_t), st));
     if (!v->d_scan) {
-        CUDA_TRY(cudaMalloc(&v->d_scan, 4104 * sizeof(uint64_t)));
-        CUDA_TRY(cudaMalloc(&v->d_counter, 4 * sizeof(unsigned long long)));
+        CUDA_TRY(dalloc(&v->d_scan, 4104 * sizeof(uint64_t), st));
+        CUDA_TRY(dalloc(&v->d_counter, 4 * sizeof(unsigned long long), st));
     }
     if (entries_need + 64 > v->entries_cap) {
-        cudaStreamSynchronize(st);
-        cudaFree(v->d_entries);
-        v->d_entries = nullptr;
+        if (v->d_entries) CUDA_TRY(cudaDeviceSynchronize());
+        dfree(v->d_entries);
         v->entries_cap = 0;
         uint64_t cap = entries_need + 64;
-        CUDA_TRY(cudaMalloc(&v->d_entries, cap));
+        CUDA_TRY(dalloc(&v->d_entries, cap, st));
         v->entries_cap = cap;
     }
     if (Lg > 5) {
@@ -207,10 +241,9 @@ static int ensure_plan(csv_volume* v, uint64_t n, uint64_t entries_need, int Lg,
         words = (words + 31) & ~31ull;
         int ctas = v->nsm * 2;
         if (words * ctas > v->gws_words_cap) {
-            cudaStreamSynchronize(st);
-            cudaFree(v->d_gws);
-            v->d_gws = nullptr;
-            CUDA_TRY(cudaMalloc(&v->d_gws, words * ctas * 4));
+            if (v->d_gws) CUDA_TRY(cudaDeviceSynchronize());
+            dfree(v->d_gws);
+            CUDA_TRY(dalloc(&v->d_gws, words * ctas * 4, st));
             v->gws_words_cap = words * ctas;
         }
         v->gws_stride = words;
@@ -228,6 +261,7 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
     if (!head120 || !out) return fail(CSV_E_ARG, "null argument");
     if (brick_end < brick_begin) return fail(CSV_E_ARG, "brick_end < brick_begin");
     CUDA_TRY(cudaSetDevice(device));
+    pool_init(device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     csv_volume* v = new csv_volume();
     v->device = device;
@@ -246,7 +280,7 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
     v->V.nb = n;
     // directory SoA
     size_t soa_bytes = n * (8 + 4 + 8 + 4 + 4 + 8 + 4 + 4) + 64;
-    cudaError_t ce = cudaMalloc(&v->d_soa, soa_bytes);
+    cudaError_t ce = dalloc(&v->d_soa, soa_bytes, st);
     if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "directory: %s", cudaGetErrorString(ce)); }
     uint8_t* p = (uint8_t*)v->d_soa;
     uint64_t* pal_off = (uint64_t*)p; p += 8 * n;
@@ -268,7 +302,7 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
         uint64_t pb = ((palette_len * 4 + 15) & ~15ull) + kBlobPad;
         uint64_t cb = ((coarse_len + 15) & ~15ull) + kBlobPad;
         uint64_t db = ((detail_len + 15) & ~15ull) + kBlobPad;
-        ce = cudaMalloc(&v->d_blob, pb + cb + db);
+        ce = dalloc(&v->d_blob, pb + cb + db, st);
         if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "blobs: %s", cudaGetErrorString(ce)); }
         cudaMemsetAsync(v->d_blob, 0, pb + cb + db, st);
         if (!deferred) {
@@ -281,7 +315,7 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
         v->V.coarse = v->d_blob + pb;
         v->V.detail = v->d_blob + pb + cb;
     }
-    ce = cudaMalloc(&v->d_dtab, 8192 * 4);
+    ce = dalloc(&v->d_dtab, 8192 * 4, st);
     if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "tables"); }
     cudaMemcpyAsync(v->d_dtab, dtab.data(), 8192 * 4, cudaMemcpyHostToDevice, st);
     v->V.dtab = v->d_dtab;
@@ -289,7 +323,7 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
         const uint8_t* ddir = dir44;
         uint8_t* tmp = nullptr;
         if (!dir_on_device) {
-            ce = cudaMalloc(&tmp, n * 44);
+            ce = dalloc(&tmp, n * 44, st);
             if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "directory staging"); }
             cudaMemcpyAsync(tmp, dir44, n * 44, cudaMemcpyHostToDevice, st);
             ddir = tmp;
@@ -298,23 +332,22 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
                                                                coarse_len, detail_base, detail_len, pal_off, pal_n,
                                                                c_off, c_bytes, c_nib, d_off, d_bytes, d_nib);
         unsigned long long* stats = nullptr;
-        cudaMalloc(&stats, 24);
+        dalloc(&stats, 24, st);
         cudaMemsetAsync(stats, 0, 24, st);
         k_region_stats<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v->V, stats, stats + 1);
         unsigned long long hs[3] = {0, 0, 0};
         cudaMemcpyAsync(hs, stats, 24, cudaMemcpyDeviceToHost, st);
+        cudaFreeAsync(stats, st);
+        if (tmp) cudaFreeAsync(tmp, st);
         ce = cudaStreamSynchronize(st);
-        cudaFree(stats);
-        if (tmp) cudaFree(tmp);
         if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_CUDA, "create: %s", cudaGetErrorString(ce)); }
         v->region_total_t0 = hs[0];
         v->region_max_t0 = hs[1];
         v->V.max_pal = (uint32_t)(hs[2] < 0xffffffffull ? hs[2] : 0xffffffffull);
     }
-    if (deferred) {  // the zero fill must land before uploads issued on other streams
-        ce = cudaStreamSynchronize(st);
-        if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_CUDA, "create: %s", cudaGetErrorString(ce)); }
-    }
+    // pool allocations, the zero fill and the uploads must land before other streams use them
+    ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_CUDA, "create: %s", cudaGetErrorString(ce)); }
     *out = v;
     return CSV_OK;
 }
@@ -386,13 +419,13 @@ int csv_volume_stage_detail(csv_volume* vol, const uint32_t* d_bricks, const uin
     }
     if (!vol->V.entropy && vol->V.nb) {   // raw streams: entry regions depend on the stream bytes
         unsigned long long* stats = nullptr;
-        CUDA_TRY(cudaMalloc(&stats, 24));
+        CUDA_TRY(dalloc(&stats, 24, st));
         cudaMemsetAsync(stats, 0, 24, st);
         k_region_stats<<<(unsigned)((vol->V.nb + 255) / 256), 256, 0, st>>>(vol->V, stats, stats + 1);
         unsigned long long hs[3] = {0, 0, 0};
         cudaMemcpyAsync(hs, stats, 24, cudaMemcpyDeviceToHost, st);
+        cudaFreeAsync(stats, st);
         cudaError_t ce = cudaStreamSynchronize(st);
-        cudaFree(stats);
         if (ce != cudaSuccess) return fail(CSV_E_CUDA, "stage: %s", cudaGetErrorString(ce));
         vol->region_total_t0 = std::max<uint64_t>(vol->region_total_t0, hs[0]);
         vol->region_max_t0 = std::max<uint64_t>(vol->region_max_t0, hs[1]);
