@@ -21,6 +21,8 @@
 #include <vector>
 #include <algorithm>
 #include <mutex>
+#include <chrono>
+#include <cstdlib>
 #include "csv_device.cuh"
 
 namespace csv {
@@ -639,8 +641,17 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
     const EncLayout Y_ = enc_layout(N);
     const size_t smem_bytes = (size_t)Y_.words * 4;
     uint64_t per_brick = ent_stride + need_stride * 4 + pal_stride * 4 + 32 + (smem ? 0 : (uint64_t)Y_.words * 4);
+    // CSVGPU_ENC_TRACE=1: host-clock phase times on stderr (encode timing investigations)
+    static const bool trace = std::getenv("CSVGPU_ENC_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what, long long k) {
+        if (!trace) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        std::fprintf(stderr, "[enc] %8.2f ms  %s %lld\n", ms, what, k);
+    };
     size_t freeb = 0, totb = 0;
     cudaMemGetInfo(&freeb, &totb);
+    mark("meminfo", 0);
     uint64_t budget = std::min<uint64_t>((uint64_t)(freeb * 0.35), 2ull << 30);
     uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, budget / per_brick));
     chunk = std::min<uint64_t>(chunk, 65536);
@@ -671,6 +682,7 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
     ETRY(reserve(&Sc.hist, &Sc.cap[8], 32 * 8));
     ETRY(cudaMalloc(&enc->d_dir, n * 44 + 16));
     if (smem) ETRY(cudaFuncSetAttribute(e12_bricks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    mark("scratch reserved, chunk", (long long)chunk);
 
     EncView E{};
     E.vol = d_volume; E.width = width; E.X = X; E.Y = Y; E.Z = Z; E.N = N; E.gx = gx; E.gy = gy; E.gz = gz;
@@ -701,6 +713,7 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
         unsigned long long h[32];
         ETRY(cudaMemcpyAsync(h, Sc.hist, sizeof h, cudaMemcpyDeviceToHost, st));
         ETRY(cudaStreamSynchronize(st));
+        mark("prepass", (long long)ids.size());
         for (int s = 0; s < 32; ++s) h[s] += 1;   // +1 smoothing (rans.py:115-116)
         quantize(h, icnt);
         quantize(h + 16, lcnt);
@@ -733,6 +746,7 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
         ETRY(cudaMemcpyAsync(&h[1], Sc.offs + 2 * V.nb, 8, cudaMemcpyDeviceToHost, st));
         ETRY(cudaMemcpyAsync(&h[2], Sc.offs + 3 * V.nb, 8, cudaMemcpyDeviceToHost, st));
         ETRY(cudaStreamSynchronize(st));
+        mark("chunk sized", (long long)c0);
         uint64_t tp = h[0], tc = h[1] - h[0], td = h[2] - h[1];
         // offsets of parts 1 and 2 are relative to the start of the whole scan: subtract in the kernel via bases
         if (c0 == 0 && V.nb < n) {   // size the blobs once from the first chunk (+12.5 %), not by regrowth
@@ -748,8 +762,10 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
                                                       enc->d_pal, enc->d_coarse, enc->d_detail, enc_doff);
         ETRY(cudaGetLastError());
         pos[0] += tp; pos[1] += tc; pos[2] += td;
+        mark("chunk assembled", (long long)c0);
     }
     ETRY(cudaStreamSynchronize(st));
+    mark("done", 0);
     enc->sizes[0] = pos[0]; enc->sizes[1] = pos[1]; enc->sizes[2] = pos[2];
     // head (container.py:235-253)
     uint8_t* hd = enc->head;
