@@ -11,6 +11,7 @@
 #include <vector>
 #include <algorithm>
 #include <mutex>
+#include <cstdlib>
 #include "csv_device.cuh"
 
 namespace csv {
@@ -170,7 +171,8 @@ static int parse_head(const uint8_t* h, csv_volume* v, uint32_t* dtab_host) {
 }
 
 // Volume memory comes from the device's default stream-ordered pool, which keeps up
-// to kPoolKeep bytes of freed blocks mapped for the next volume: a host-in/host-out
+// to kPoolKeep bytes (env CSVGPU_POOL_KEEP_GB overrides) of freed blocks mapped for
+// the next volume: a host-in/host-out
 // decompress_volume creates and frees a ~2 GB volume per call, and plain
 // cudaMalloc/cudaFree of that made every call pay 10-850 ms of driver page mapping.
 // Frees follow a device synchronisation (the cudaFree semantics the callers rely on).
@@ -184,6 +186,7 @@ static void pool_init(int device) {
         cudaMemPool_t mp;
         if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
             uint64_t keep = kPoolKeep;
+            if (const char* g = std::getenv("CSVGPU_POOL_KEEP_GB")) keep = (uint64_t)(std::atof(g) * (1ull << 30));
             cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
         }
     });
