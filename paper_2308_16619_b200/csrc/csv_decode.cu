@@ -127,6 +127,7 @@ struct Lane {
     uint4 nq;               // prefetched chunk
     uint64_t buf;           // upcoming stream bits, MSB first
     uint32_t alo, ahi;      // last <= 8 entry bytes, newest in the top byte of ahi
+    uint32_t plo, phi;      // the previous complete 8-entry group (stored in 16-byte pairs)
     uint64_t* outp;         // entry region (32-byte aligned)
     uint64_t c03, c47;      // count mode: per-op counters, 4 x 16 bits each
     const uint8_t* rawp;    // raw mode: packed nibble bytes
@@ -192,13 +193,17 @@ __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
         // 8 appends the first entry sits in the lowest byte (little-endian order)
         L.alo = __byte_perm(L.alo, L.ahi, 0x4321);
         L.ahi = __byte_perm(L.ahi, L.cur, 0x4321);
-        if ((++L.ne & 7u) == 0u) L.outp[(L.ne >> 3) - 1] = ((uint64_t)L.ahi << 32) | L.alo;
+        if ((++L.ne & 7u) == 0u) {
+            if (L.ne & 8u) { L.plo = L.alo; L.phi = L.ahi; }   // first group of a pair: hold it
+            else reinterpret_cast<uint4*>(L.outp)[(L.ne >> 4) - 1] = make_uint4(L.plo, L.phi, L.alo, L.ahi);
+        }
     }
 }
 
 __device__ __forceinline__ void lane_finish(Lane& L, const Plan& P, bool failed, bool entropy) {
     if (P.op_counts) lane_flush_counts(L, P.op_counts);
-    else if (L.ne & 7u) {   // partial group: move its entries down to byte 0, zero above
+    else if (L.ne & 8u) L.outp[(L.ne >> 3) - 1] = ((uint64_t)L.phi << 32) | L.plo;   // unpaired last group
+    if (!P.op_counts && (L.ne & 7u)) {   // partial group: move its entries down to byte 0, zero above
         const uint64_t a = ((uint64_t)L.ahi << 32) | L.alo;
         L.outp[L.ne >> 3] = a >> (8 * (8 - (L.ne & 7u)));
     }
