@@ -195,7 +195,7 @@ __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
         L.ahi = __byte_perm(L.ahi, L.cur, 0x4321);
         if ((++L.ne & 7u) == 0u) {
             if (L.ne & 8u) { L.plo = L.alo; L.phi = L.ahi; }   // first group of a pair: hold it
-            else reinterpret_cast<uint4*>(L.outp)[(L.ne >> 4) - 1] = make_uint4(L.plo, L.phi, L.alo, L.ahi);
+            else __stcs(reinterpret_cast<uint4*>(L.outp) + ((L.ne >> 4) - 1), make_uint4(L.plo, L.phi, L.alo, L.ahi));
         }
     }
 }
