@@ -188,15 +188,17 @@ __device__ __forceinline__ void lane_emit(Lane& L, uint32_t s) {
         return;
     }
     L.cur = pay ? (L.cur | (s << 4)) : s;
-    if (!L.pend) {
-        // shift the 8-byte window down one byte and append the entry on top: after
-        // 8 appends the first entry sits in the lowest byte (little-endian order)
-        L.alo = __byte_perm(L.alo, L.ahi, 0x4321);
-        L.ahi = __byte_perm(L.ahi, L.cur, 0x4321);
-        if ((++L.ne & 7u) == 0u) {
-            if (L.ne & 8u) { L.plo = L.alo; L.phi = L.ahi; }   // first group of a pair: hold it
-            else __stcs(reinterpret_cast<uint4*>(L.outp) + ((L.ne >> 4) - 1), make_uint4(L.plo, L.phi, L.alo, L.ahi));
-        }
+    // shift the 8-byte window down one byte and append the entry on top (after 8
+    // appends the first entry sits in the lowest byte, little-endian order); selects
+    // instead of a branch on the payload flag, which diverges within a warp
+    const bool em = !L.pend;
+    const uint32_t nlo = __byte_perm(L.alo, L.ahi, 0x4321), nhi = __byte_perm(L.ahi, L.cur, 0x4321);
+    L.alo = em ? nlo : L.alo;
+    L.ahi = em ? nhi : L.ahi;
+    L.ne += em ? 1u : 0u;
+    if (em && (L.ne & 7u) == 0u) {
+        if (L.ne & 8u) { L.plo = L.alo; L.phi = L.ahi; }   // first group of a pair: hold it
+        else __stcs(reinterpret_cast<uint4*>(L.outp) + ((L.ne >> 4) - 1), make_uint4(L.plo, L.phi, L.alo, L.ahi));
     }
 }
 
