@@ -8,7 +8,7 @@
 //                     one single-state rANS chain (codec.py:290-300), decodes it
 //                     with the packed 4096-entry decode table in shared memory,
 //                     parses op/payload nibbles into one entry byte per
-//                     operation and stores them 8 at a time.  Lanes refill
+//                     operation and stores them 16 at a time.  Lanes refill
 //                     work dynamically from a global counter (warp-aggregated
 //                     atomics), detail streams (long) first.
 //  K2w k2_warp     -- replay stage (csv_replay_warp.cuh), the default: one
