@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_streams(VolView V, Plan P
                 if (L.slow && !lane_step<ENTROPY, COUNT, true, true>(L, P, tab)) has = false;
                 if (has) {
 #pragma unroll 8
-                    for (int u = 0; u < 16; ++u) {
+                    for (int u = 0; u < 32; ++u) {
                         if (L.nb < 32) lane_refill(L);
                         if (!lane_step<ENTROPY, COUNT, false, false>(L, P, tab)) { has = false; break; }
                         if (!lane_step<ENTROPY, COUNT, false, false>(L, P, tab)) { has = false; break; }
