@@ -10,15 +10,19 @@ Workload (BASELINE.json north_star / configs[2]):
 One step = one full-volume decode at LOD 0 of this rank's brick range (K1
 entropy lanes + K2 replay/raster writer) from HBM-resident compressed data
 into an HBM-resident (Z,Y,X) uint32 output.  Output (34 GB) and input
-(~1.5 GB) both exceed the 126 MB L2, so no flush is needed between steps.
+(~0.9 GB) both exceed the 126 MB L2, so no flush is needed between steps.
 
-Multi-GPU (--gpus N under torchrun): bricks are independent, so the job shards
-them with no data-path collective.  Default --scaling weak: every rank decodes its
-own config-3 volume (seed 2 + rank), value = N x 2048^3 / max-over-ranks time.
---scaling strong splits ONE 2048^3 volume into whole-bz-layer ranges instead.
+Multi-GPU (--gpus N under torchrun), north_star's configuration by default
+(--scaling strong): ONE 2048^3 volume, its brick index range-partitioned in
+whole bz layers over the ranks (distributed.rank_bricks); value = 2048^3 /
+max-over-ranks decode time.  The decoded slabs' gather to rank 0 (grouped
+ncclSend/ncclRecv into the root's volume) and to every rank
+(all_gather_into_tensor) are timed separately ("decode_gather").
+--scaling weak (one volume per rank) is kept as a labelled extra.
 
-`--impl reference` times the reference's CPU algorithm (oracle/ C port, all
-host threads) on a bounded sample of the same workload.
+`--impl reference` times the reference itself (csvol from baseline/_ref, its
+numba decoder through decompress_volume(workers=all host cores)) on a bounded
+sample of the same workload; the oracle's C port is timed beside it.
 """
 
 from __future__ import annotations
@@ -59,8 +63,9 @@ def parse_args():
     ap.add_argument("--no-cache", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
     ap.add_argument("--zlayers", type=int, default=0, help="profiling: only the first K bz-layers of the volume")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: one volume per rank (default); strong: one volume split across ranks")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): one volume range-partitioned over the ranks; weak: one volume per rank")
+    ap.add_argument("--no-gather", action="store_true", help="skip the decode+gather timing")
     return ap.parse_args()
 
 
@@ -146,60 +151,205 @@ def max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(v: int, world: int) -> int:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t)
+    return int(t.item())
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
 
 
-# ---------------------------------------------------------------------------- CPU baseline (oracle)
-def cpu_baseline(wl, target_s: float = 12.0, layers_cap: int = 8):
-    """Reference CPU decoder (oracle C port, all host threads) on the first bz-layers of the workload."""
+# ---------------------------------------------------------------------------- CPU baselines
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def import_csvol():
+    """The reference package from baseline/_ref (pip --target install of /root/reference),
+    or (None, why)."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "csvol_numba_cache"))
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "csvol")):
+        return None, "baseline/_ref/csvol not installed"
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import csvol
+        import csvol.cli
+        return csvol, None
+    except Exception as e:   # numba missing etc.
+        return None, f"{type(e).__name__}: {e}"
+
+
+def sample_volume(wl, layers: int, cores: int):
+    """First `layers` bz-layers of the workload's volume (oracle generator, same field as the GPU one)."""
     from oracle import oracle as orc
     orc.build()
-    cores = len(os.sched_getaffinity(0))
     X, Y, Z = wl["dims"]
-    b = 1 << BRICK_LOG2
+    zs = min(layers << BRICK_LOG2, Z)
+    # rows [0, zs] (+1 row so membranes of the last row see their +z neighbour)
+    return orc.synth_voronoi((X, Y, Z), wl["cells"], wl["seed"], wl["membrane"],
+                             z_range=(0, min(zs + 1, Z)), threads=cores)[:zs]
 
-    def make(layers):
-        zs = min(layers * b, Z)
-        # rows [0, zs] (+1 row so membranes of the last row see their +z neighbour)
-        rows = orc.synth_voronoi((X, Y, Z), wl["cells"], wl["seed"], wl["membrane"],
-                                 z_range=(0, min(zs + 1, Z)), threads=cores)[:zs]
-        return orc.compress_volume(np.ascontiguousarray(rows), brick_log2=BRICK_LOG2, threads=cores), zs
 
-    c1, zs = make(1)
-    t0 = time.perf_counter()
-    orc.decompress_volume(c1, 0, threads=cores)
-    one = time.perf_counter() - t0
-    layers = max(1, min(layers_cap, int(target_s / 3 / max(one, 1e-3))))
-    c, zs = make(layers) if layers > 1 else (c1, zs)
-    best = float("inf")
-    for _ in range(3):
+def port_decode_baseline(wl, cores: int, layers: int = 8, reps: int = 3):
+    """The oracle's C restatement of _decode_kernel + morton_to_grid, OpenMP over bricks."""
+    from oracle import oracle as orc
+    vol = sample_volume(wl, layers, cores)
+    c = orc.compress_volume(np.ascontiguousarray(vol), brick_log2=BRICK_LOG2, threads=cores)
+    X, Y, _ = wl["dims"]
+    times = []
+    for _ in range(reps):
         t0 = time.perf_counter()
         bad, _, _ = orc.decompress_volume(c, 0, threads=cores)
-        best = min(best, time.perf_counter() - t0)
+        times.append(time.perf_counter() - t0)
         assert bad == -1
-    vox = X * Y * zs
-    return {"value": vox / best / 1e9, "unit": "GVoxel/s", "cores": cores, "kind": "port",
-            "sample": f"first {layers} bz-layer(s) ({X}x{Y}x{zs} = {vox / 1e6:.0f} MVox) of the workload, "
-                      f"oracle-encoded; oracle decompress_volume (C restatement of _decode_kernel + "
-                      f"morton_to_grid placement), {cores} OpenMP threads, best of 3"}
+    vox = vol.size
+    return {"value": vox / min(times) / 1e9, "unit": "GVoxel/s", "cores": cores, "kind": "port",
+            "sample": f"first {layers} bz-layer(s) ({X}x{Y}x{vol.shape[0]} = {vox / 1e6:.0f} MVox); "
+                      f"oracle/ C port of _decode_kernel + morton_to_grid, {cores} OpenMP threads, best of {reps}"}, c
+
+
+def csvol_container(csvol, orc_container):
+    return csvol.CsvContainer.from_bytes(orc_container.to_bytes())
+
+
+def reference_decode(csvol, c, vox: int, workers: int, reps: int):
+    """csvol.decompress_volume(c, 0, workers=W) timed as cli.py:125-169 times it
+    (JIT warmed by cli._warm_kernels, perf_counter, best of reps)."""
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        csvol.decompress_volume(c, 0, workers=workers)
+        times.append(time.perf_counter() - t0)
+    return vox / min(times) / 1e9, times
+
+
+def reference_cache_frame(csvol, c, reqs, n_sample: int):
+    """Config 4 on the reference's own path: BrickCache.end_frame_assign with
+    CsvContainer.decode_brick as the decode hook (cache.py:139-170,
+    render.py:876-885), serial by construction, on the first n_sample requests."""
+    sub = reqs[:n_sample]
+    cache = csvol.BrickCache(c.meta.brick_count, BRICK_LOG2, pool_bytes=4 << 30)
+    cache.begin_frame()
+    for b, l in sub:
+        cache.mark_used(b, l)
+    t0 = time.perf_counter()
+    placed = cache.end_frame_assign(sub, lambda b, l: c.decode_brick(b, l))
+    dt = time.perf_counter() - t0
+    vox = sum(8 ** (BRICK_LOG2 - l) for _, l in placed)
+    return {"value": vox / dt / 1e9, "unit": "GVoxel/s", "requests": len(sub), "seconds": dt,
+            "us_per_brick": dt / max(len(sub), 1) * 1e6,
+            "sample": f"the {len(sub)} nearest of config 4's 65,536 requests (all in the first bz-layers), "
+                      f"one end_frame_assign into an empty pool, serial"}
+
+
+def reference_compress(csvol, wl5, cores: int, layers: int = 1):
+    """Config 5 encode on the reference: compress_volume(workers=all) (container.py:374-453)
+    on the first bz-layer(s) of timestep 0."""
+    from oracle import oracle as orc
+    X, Y, Z = wl5["dims"]
+    zs = min(layers << BRICK_LOG2, Z)
+    vol = orc.synth_voronoi((X, Y, Z), wl5["cells"], wl5["seed"], False, z_range=(0, zs), threads=cores)
+    t0 = time.perf_counter()
+    csvol.compress_volume(vol, csvol.CompressionConfig(brick_log2=BRICK_LOG2, workers=cores))
+    dt = time.perf_counter() - t0
+    return {"value": vol.size / dt / 1e9, "unit": "GVoxel/s", "seconds": dt, "cores": cores,
+            "sample": f"compress_volume of the first {layers} bz-layer(s) of a config-5 timestep "
+                      f"({X}x{Y}x{zs}), workers={cores}"}
+
+
+def cpu_baselines(wl, cache_reqs=None):
+    """Every CPU number the line carries (rank 0, N=1): the reference (csvol) decoder at
+    W = all cores (the headline baseline) and W = 1, its cache path (config 4) and
+    encoder (config 5), and the oracle's C port."""
+    cores = len(os.sched_getaffinity(0))
+    out = {"cpu_model": cpu_model()}
+    port, pc = port_decode_baseline(wl, cores)
+    csvol, why = import_csvol()
+    if csvol is None:
+        port["reference_unavailable"] = why
+        port["cpu_model"] = out["cpu_model"]
+        return port
+    csvol.cli._warm_kernels()
+    X, Y, _ = wl["dims"]
+    from oracle import oracle as orc
+    vol2 = sample_volume(wl, 2, cores)
+    c2 = csvol_container(csvol, orc.compress_volume(np.ascontiguousarray(vol2), brick_log2=BRICK_LOG2, threads=cores))
+    vall, tall = reference_decode(csvol, c2, vol2.size, cores, 3)
+    vol1 = vol2[: 1 << BRICK_LOG2]
+    c1 = csvol_container(csvol, orc.compress_volume(np.ascontiguousarray(vol1), brick_log2=BRICK_LOG2, threads=cores))
+    v1, t1 = reference_decode(csvol, c1, vol1.size, 1, 1)
+    line = {"value": vall, "unit": "GVoxel/s", "cores": cores, "kind": "reference",
+            "sample": f"first 2 bz-layers ({X}x{Y}x{vol2.shape[0]} = {vol2.size / 1e6:.0f} MVox); "
+                      f"csvol.decompress_volume(c, 0, workers={cores}) from baseline/_ref (numba, JIT warmed), "
+                      f"best of 3: {[round(x, 3) for x in tall]} s",
+            "cpu_model": out["cpu_model"],
+            "w1": {"value": v1, "unit": "GVoxel/s", "cores": 1, "seconds": t1[0],
+                   "sample": f"first bz-layer ({vol1.size / 1e6:.0f} MVox), workers=1"},
+            "port": port}
+    if cache_reqs:
+        line["cache_path"] = reference_cache_frame(csvol, c2, [r for r in cache_reqs if r[0] < c2.meta.brick_count],
+                                                   4096)
+    line["compress"] = reference_compress(csvol, WORKLOADS["config2"] | {"seed": 3}, cores)
+    return line
 
 
 def run_reference(args, world, rank):
+    """The reference arm: csvol's own decoder (baseline/_ref) on the host cores, W + K
+    steps of one decompress_volume(workers=all) over a 2-bz-layer sample each."""
     if rank != 0:
         return
     wl = WORKLOADS[args.workload]
-    cb = cpu_baseline(wl)
+    cores = len(os.sched_getaffinity(0))
     X, Y, Z = wl["dims"]
-    line = {"impl": "reference", "metric": "decoded GVoxel/s (full-volume decode, LOD 0)", "value": cb["value"],
+    csvol, why = import_csvol()
+    from oracle import oracle as orc
+    vol = sample_volume(wl, 2, cores)
+    oc = orc.compress_volume(np.ascontiguousarray(vol), brick_log2=BRICK_LOG2, threads=cores)
+    if csvol is not None:
+        csvol.cli._warm_kernels()
+        c = csvol_container(csvol, oc)
+        step = lambda: csvol.decompress_volume(c, 0, workers=cores)   # noqa: E731
+        kind, what = "reference", f"csvol.decompress_volume(c, 0, workers={cores}) (baseline/_ref, numba)"
+    else:
+        step = lambda: orc.decompress_volume(oc, 0, threads=cores)   # noqa: E731
+        kind, what = "port", f"oracle C port, {cores} OpenMP threads (csvol unavailable: {why})"
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    ms = statistics.mean(times) * 1e3
+    value = vol.size / (ms * 1e-3) / 1e9
+    sample = (f"each step decodes the first 2 bz-layers of the workload ({X}x{Y}x{vol.shape[0]} = "
+              f"{vol.size / 1e6:.0f} MVox of the {X * Y * Z / 1e6:.0f} MVox volume); {what}")
+    line = {"impl": "reference", "metric": "decoded GVoxel/s (full-volume decode, LOD 0)", "value": value,
             "unit": "GVoxel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": X * Y * Z / (cb["value"] * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": wl["desc"], "brick": 32, "entropy": "rANS", "lod": 0},
-            "cpu_baseline": cb,
-            "e2e": {"value": cb["value"], "unit": "GVoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": {"workload": wl["desc"], "brick": 32, "entropy": "rANS", "lod": 0,
+                                            "sample_voxels_per_step": int(vol.size)},
+            "step_seconds": [round(x, 4) for x in times],
+            "cpu_baseline": {"value": value, "unit": "GVoxel/s", "cores": cores, "kind": kind, "sample": sample,
+                             "cpu_model": cpu_model()},
+            "e2e": {"value": value, "unit": "GVoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -257,10 +407,57 @@ def timeseries_leg(p, torch, dev, stream, steps: int = 2, dims=(1024, 1024, 1024
 
 
 # ---------------------------------------------------------------------------- our arm
+def strong_rank_plan(dims, brick_log2: int, world: int, rank: int) -> dict:
+    """This rank's share of ONE volume (north_star / SURVEY.md §8e): whole bz layers,
+    contiguous brick range and LOD-0 raster rows."""
+    from paper_2308_16619_b200.distributed import rank_bricks, rank_slab
+    X, Y, Z = dims
+    b = 1 << brick_log2
+    grid = (-(-X // b), -(-Y // b), -(-Z // b))
+    b0, b1 = rank_bricks(grid, world, rank)
+    z0, z1 = rank_slab(dims, brick_log2, 0, world, rank)
+    return {"bricks": (b0, b1), "rows": (z0, z1), "layers": (b0 // (grid[0] * grid[1]), b1 // (grid[0] * grid[1])),
+            "voxels": (z1 - z0) * Y * X}
+
+
+def sample_bricks(vol, grid, n: int = 64, seed: int = 7):
+    """A fixed sample of brick indices with their raster blocks (cropped), kept on the host
+    to verify the timed output after the run."""
+    gx, gy, gz = grid
+    rng = np.random.default_rng(seed)
+    idx = np.unique(np.concatenate([[0, gx * gy * gz - 1], rng.integers(0, gx * gy * gz, n - 2)]))
+    b = 1 << BRICK_LOG2
+    blocks = {}
+    for i in idx.tolist():
+        bx, by, bz = i % gx, i // gx % gy, i // (gx * gy)
+        blocks[i] = vol[bz * b:(bz + 1) * b, by * b:(by + 1) * b, bx * b:(bx + 1) * b].cpu()
+    return blocks
+
+
+def check_bricks(blocks, out, z_first: int, brick_lo: int, brick_hi: int, grid) -> dict:
+    """Compare the sampled bricks inside [brick_lo, brick_hi) with `out` (rows from z_first)."""
+    gx, gy, _ = grid
+    b = 1 << BRICK_LOG2
+    n = bad = 0
+    for i, ref in blocks.items():
+        if not brick_lo <= i < brick_hi:
+            continue
+        bx, by, bz = i % gx, i // gx % gy, i // (gx * gy)
+        got = out[bz * b - z_first:(bz + 1) * b - z_first, by * b:(by + 1) * b, bx * b:(bx + 1) * b].cpu()
+        n += 1
+        bad += 0 if torch_equal(got, ref) else 1
+    return {"bricks_checked": n, "mismatches": bad}
+
+
+def torch_equal(a, b) -> bool:
+    import torch
+    return a.shape == b.shape and bool(torch.equal(a, b))
+
+
 def run_ours(args, world, rank, local):
     import torch
     import paper_2308_16619_b200 as p
-    from paper_2308_16619_b200.distributed import bz_range
+    from paper_2308_16619_b200.distributed import gather_slabs
     wl = dict(WORKLOADS[args.workload])
     if args.zlayers:
         wl["dims"] = (wl["dims"][0], wl["dims"][1], 32 * args.zlayers)
@@ -269,34 +466,42 @@ def run_ours(args, world, rank, local):
     dev = torch.device("cuda", local)
     hbm, peak_kind = peaks()
     b = 1 << BRICK_LOG2
-    gx, gy, gz = (-(-X // b), -(-Y // b), -(-Z // b))
-    # ---- data: GPU synth + GPU encode (untimed)
-    t0 = time.perf_counter()
+    grid = gx, gy, gz = (-(-X // b), -(-Y // b), -(-Z // b))
     weak = args.scaling == "weak"
+    # ---- data: GPU synth + GPU encode (untimed); strong: every rank builds the same volume
+    t0 = time.perf_counter()
     seed = wl["seed"] + (rank if weak else 0)
     vol = p.synth_voronoi((X, Y, Z), wl["cells"], seed, wl["membrane"], device=dev)
     torch.cuda.synchronize()
     t_synth = time.perf_counter() - t0
+    blocks = sample_bricks(vol, grid)
     t0 = time.perf_counter()
     enc = p.compress_volume_device(vol, p.CompressionConfig(brick_log2=BRICK_LOG2))
     torch.cuda.synchronize()
     t_enc = time.perf_counter() - t0
     del vol
     torch.cuda.empty_cache()
-    z0b, z1b = (0, gz) if weak else bz_range(gz, world, rank)
-    brick_range = (z0b * gx * gy, z1b * gx * gy)
+    plan = strong_rank_plan((X, Y, Z), BRICK_LOG2, 1 if weak else world, 0 if weak else rank)
+    brick_range = plan["bricks"]
+    zr = plan["rows"]
     gv = enc.to_volume(brick_range)
-    zr = gv.slab(0)
-    out = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32, device=dev)
-    res = torch.empty((gv.n_bricks, 4), dtype=torch.int64, device=dev)
-    voxels_rank = (zr[1] - zr[0]) * Y * X
+    root = rank == 0
+    # the root holds the whole volume (strong) and decodes its slab straight into its rows
+    full = None
+    if not weak and root:
+        full = torch.empty((Z, Y, X), dtype=torch.int32, device=dev)
+        out = full[zr[0]:zr[1]]
+    else:
+        out = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32, device=dev)
+    res = torch.empty((max(gv.n_bricks, 1), 4), dtype=torch.int64, device=dev)
+    voxels_rank = plan["voxels"]
     voxels_all = X * Y * Z * (world if weak else 1)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         gv.decode(0, out=out, results=res)
     torch.cuda.synchronize()
     p.GpuVolume.raise_first(res, gv.n_bricks)
-    # ---- timed region
+    # ---- timed region: decode only
     clocks = Clocks(local)
     if not args.profile:
         clocks.start()
@@ -315,6 +520,48 @@ def run_ours(args, world, rank, local):
     p.GpuVolume.raise_first(res, gv.n_bricks)
     ms = max_over_ranks(ms_rank, world)
     value = voxels_all / (ms * 1e-3) / 1e9
+    check = check_bricks(blocks, out, zr[0], brick_range[0], brick_range[1], grid)
+    # ---- decode + gather (strong): the slabs to the root's volume (grouped send/recv), and
+    # to every rank (all_gather_into_tensor); at N = 1 the gather is a no-op
+    gather = None
+    if not weak and not args.no_gather and not args.profile:
+        gather = {}
+        for mode in ("root", "all"):
+            if mode == "all" and world > 1 and not root:
+                vol_all = torch.empty((Z, Y, X), dtype=torch.int32, device=dev)
+            else:
+                vol_all = full
+            dst = vol_all[zr[0]:zr[1]] if vol_all is not None and (mode == "all" or root) else out
+
+            def step():
+                gv.decode(0, out=dst, results=res)
+                if world > 1:
+                    gather_slabs(dst, vol_all if (mode == "all" or root) else None, (X, Y, Z), BRICK_LOG2, 0,
+                                 mode=mode, root=0)
+            step()
+            torch.cuda.synchronize()
+            barrier(world)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(args.steps):
+                step()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            barrier(world)
+            gms = max_over_ranks(g0.elapsed_time(g1) / args.steps, world)
+            ent = {"value": X * Y * Z / (gms * 1e-3) / 1e9, "unit": "GVoxel/s", "ms_per_step": gms,
+                   "gather_bytes_per_rank": 4 * (X * Y * Z - voxels_rank) if mode == "all" else
+                   (4 * (X * Y * Z - voxels_rank) if root else 4 * voxels_rank),
+                   "collective": ("none (N = 1)" if world == 1 else
+                                  "batch_isend_irecv: grouped ncclSend/ncclRecv of each slab into the root's "
+                                  "(Z,Y,X) rows" if mode == "root" else
+                                  "all_gather_into_tensor into each rank's (Z,Y,X) volume")}
+            if mode == "root" and root:
+                ent["check"] = check_bricks(blocks, full, 0, 0, gx * gy * gz, grid)
+            gather[mode] = ent
+            if mode == "all" and world > 1 and not root:
+                del vol_all
+                torch.cuda.empty_cache()
     # ---- per-stage timing (CUDA events on the launching stream, separate pass)
     gv.set_timing(True)
     stages = []
@@ -323,34 +570,34 @@ def run_ours(args, world, rank, local):
         stages.append(gv.last_timing())
     gv.set_timing(False)
     plan_ms, k1_ms, k2_ms = (statistics.median(s[i] for s in stages) for i in range(3))
-    # ---- algorithmic bytes for this rank's bricks
-    cont = enc.to_container() if rank == 0 or world == 1 else enc.to_container()
+    # ---- algorithmic bytes for this rank's bricks, split by kernel:
+    # K1 reads the coarse/detail streams + directory, K2w the palettes + directory and
+    # writes the voxels.  K1's entry bytes are an intermediate and count for neither.
+    cont = enc.to_container()
     d = cont.directory[brick_range[0]:brick_range[1]]
     pal_b = 4 * int(d["palette_len"].sum())
     cb_b = int(d["coarse_bytes"].sum())
     db_b = int(d["detail_bytes"].sum())
     n_b = brick_range[1] - brick_range[0]
     step_bytes = pal_b + cb_b + db_b + 44 * n_b + 64 + 4 * voxels_rank
-    ent, offs, sres = gv.decode_streams(torch.arange(brick_range[0], brick_range[1], dtype=torch.int32,
-                                                     device=dev), 0)
-    entries = int(sres[:, 0].to(torch.int64).sum())
-    k1_bytes = cb_b + db_b + entries + 44 * n_b
-    k2_bytes = entries + pal_b + 44 * n_b + 4 * voxels_rank
-    del ent, offs, sres
-    dom = ("k2_replay", k2_ms, k2_bytes) if k2_ms >= k1_ms else ("k1_streams", k1_ms, k1_bytes)
-    long_pal = int(d["palette_len"].max()) > 256 if n_b else False      # K2w runs a second (u16) pass
-    traffic = None
+    k1_bytes = cb_b + db_b + 44 * n_b + 64
+    k2_bytes = pal_b + 44 * n_b + 4 * voxels_rank
+    traffic = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tj = json.load(f)
-        if tj.get("workload") == args.workload and not args.zlayers and (world == 1 or args.scaling == "weak"):
-            traffic = tj.get(dom[0])
+        if tj.get("workload") == args.workload and not args.zlayers and (world == 1 or weak):
+            traffic = tj
     except Exception:
         pass
-    achieved = dom[2] / (dom[1] * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k2_warp" if dom[0] == "k2_replay" else dom[0], "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                "algorithmic_bytes": dom[2], "kernel_ms": dom[1]}
+
+    def kline(name, kms, kbytes):
+        ach = kbytes / (kms * 1e-3) / 1e9
+        return {"bound": "hbm", "kernel": name, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": traffic.get(name), "peak_kind": peak_kind, "algorithmic_bytes": kbytes, "kernel_ms": kms}
+    kernels = {"k1_streams": kline("k1_streams", k1_ms, k1_bytes), "k2_warp": kline("k2_warp", k2_ms, k2_bytes)}
+    roofline = dict(kernels["k2_warp"] if k2_ms >= k1_ms else kernels["k1_streams"])
+    long_pal = int(d["palette_len"].max()) > 256 if n_b else False      # K2w runs a second (u16) pass
     step_gbs = step_bytes / (ms_rank * 1e-3) / 1e9
     line = {
         "metric": "decoded GVoxel/s (full-volume decode, LOD 0)", "value": value, "unit": "GVoxel/s",
@@ -358,24 +605,31 @@ def run_ours(args, world, rank, local):
         "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (GPU Voronoi generator; GPU encoder, byte-identical to the reference encoder)",
         "config": {"workload": wl["desc"], "brick": 32, "entropy": "rANS", "lod": 0, "bricks": gx * gy * gz,
-                   "compressed_bytes": int(enc.payload_bytes), "compression_rate": enc.payload_bytes / (4 * voxels_all),
+                   "compressed_bytes": int(enc.payload_bytes), "compression_rate": enc.payload_bytes / (4 * X * Y * Z),
                    "parallelism": (f"one config-3 volume per rank (seed {wl['seed']} + rank) x{world}" if weak
-                                   else f"bz-layer range per rank x{world}"),
+                                   else f"one volume, bz layers [{plan['layers'][0]}, {plan['layers'][1]}) on rank "
+                                        f"{rank} of {world} (whole-bz-layer brick ranges)"),
                    "l2": "inputs (~%.1f GB compressed) and output (%.1f GB) exceed L2; no flush" %
-                         (enc.payload_bytes / 1e9, 4 * voxels_all / 1e9)},
+                         (enc.payload_bytes / 1e9, 4 * X * Y * Z / 1e9)},
         "roofline": roofline,
+        "kernels": kernels,
         "step_roofline": {"achieved": step_gbs, "peak": hbm, "unit": "GB/s", "frac": step_gbs / hbm,
                           "algorithmic_bytes": step_bytes, "bytes_per_voxel": step_bytes / voxels_rank},
         "stages_ms": {"plan": plan_ms, "k1_streams": k1_ms, "k2_replay": k2_ms},
         "clocks": clk,
         "gpu_launches": (7 if long_pal else 6) * args.steps,   # sizes, 3 scan, K1, K2w (+ u16 K2w)
+        "check": dict(check, what="sampled bricks of the timed output vs the generated input volume"),
         "setup_s": {"synth": t_synth, "encode": t_enc},
     }
+    if gather is not None:
+        line["decode_gather"] = gather
     # ---- config 4: batched random-access decode into a device brick pool
+    cache_reqs = None
     if not args.no_cache and not args.profile and world == 1:
         lod, dist = desired_lods((gx, gy, gz), b, (1024.0, 1024.0, -64.0), math.pi / 3, 1080, BRICK_LOG2)
         order = np.argsort(dist, kind="stable")[:65536]
         reqs = [(int(i), int(lod[i])) for i in order if lod[i] < BRICK_LOG2]
+        cache_reqs = reqs
         cache = p.BrickCache(gx * gy * gz, BRICK_LOG2, pool_bytes=8 << 30, device=dev)
         cache.begin_frame()
         for br, l in reqs:
@@ -387,16 +641,16 @@ def run_ours(args, world, rank, local):
         bricks = torch.from_numpy(arr[:, 0].astype(np.int32)).to(dev)
         lods = torch.from_numpy(arr[:, 1].astype(np.uint8)).to(dev)
         dst = torch.from_numpy(arr[:, 2] * 8).to(dev)
-        full = enc.to_volume()
+        fvol = enc.to_volume()
         cres = torch.empty((len(live), 4), dtype=torch.int64, device=dev)
         for _ in range(args.warmup):
-            full.decode_bricks(bricks, lods, dst, cache.pool, results=cres)
+            fvol.decode_bricks(bricks, lods, dst, cache.pool, results=cres)
         torch.cuda.synchronize()
         p.GpuVolume.raise_first(cres, len(live))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            full.decode_bricks(bricks, lods, dst, cache.pool, results=cres)
+            fvol.decode_bricks(bricks, lods, dst, cache.pool, results=cres)
         e1.record(stream)
         torch.cuda.synchronize()
         cms = e0.elapsed_time(e1) / args.steps
@@ -417,18 +671,18 @@ def run_ours(args, world, rank, local):
         none_b = torch.empty(0, dtype=torch.int32, device=dev)
         none_l = torch.empty(0, dtype=torch.uint8, device=dev)
         cam = p.Camera(position=(1024.0, 1024.0, -64.0), fov=math.pi / 3, width=1920, height=1080)
-        dl = p.desired_lods_device(full, cam)
+        dl = p.desired_lods_device(fvol, cam)
         assert torch.equal(dl[rb.long()], rl), "device LODs differ from the restated desired_lods"
 
         def frame():
-            p.desired_lods_device(full, cam, out=dl)
+            p.desired_lods_device(fvol, cam, out=dl)
             dcache.begin_frame()
             dcache.mark_used(rb, rl)
-            return dcache.end_frame_assign(rb, rl, full)
+            return dcache.end_frame_assign(rb, rl, fvol)
 
         def evict_all():
             dcache.begin_frame()
-            dcache.end_frame_assign(none_b, none_l, full)
+            dcache.end_frame_assign(none_b, none_l, fvol)
 
         for _ in range(max(1, args.warmup)):
             evict_all()
@@ -478,7 +732,7 @@ def run_ours(args, world, rank, local):
                     "level-0 streams + batched decode; detail blob never resident on the GPU; wall clock, median"}
         cold.close()
         dcache.close()
-        full.close()
+        fvol.close()
     # ---- config 5: time series encode + decode (2 timesteps = one GPU's share of 16 over 8 GPUs)
     if not args.no_cache and not args.profile and world == 1 and args.workload == "config3" and not args.zlayers:
         line["timeseries"] = timeseries_leg(p, torch, dev, stream)
@@ -488,31 +742,32 @@ def run_ours(args, world, rank, local):
             pin = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32, pin_memory=True)
         except RuntimeError:
             pin = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32)
-        h2d = 0
         times = []
         pin_np = pin.numpy().view(np.uint32)
+        layers = None if weak else plan["layers"]
         for it in range(5):
             torch.cuda.synchronize()
+            barrier(world)
             t0 = time.perf_counter()
-            if world == 1 or weak:
-                p.decompress_volume(cont, 0, out=pin_np)     # the reference-facing API, host in / host out
-            else:
-                hv = cont.to_device(device=dev, brick_range=brick_range)
-                dout = p.decompress_volume_device(hv, 0, out=out)
-                pin.copy_(dout, non_blocking=True)
-                torch.cuda.synchronize()
-                hv.close()
+            # the reference-facing API, host container in / host (slab of the) volume out
+            p.decompress_volume(cont, 0, out=pin_np, layers=layers)
             times.append(time.perf_counter() - t0)
-            h2d = (44 * n_b + pal_b + cb_b + db_b)
         e2e_s = max_over_ranks(min(times), world)
+        h2d = sum_over_ranks(44 * n_b + pal_b + cb_b + db_b, world)
+        d2h = sum_over_ranks(4 * voxels_rank, world)
         line["e2e"] = {"value": voxels_all / e2e_s / 1e9, "unit": "GVoxel/s", "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": 4 * voxels_rank + 32 * n_b, "seconds": e2e_s,
-                       "seconds_all": [round(x, 4) for x in times], "reduction": "best of 5 (host-timed, synchronised)",
-                       "path": "decompress_volume(container, 0, out=pinned host array): H2D of directory+blobs, "
-                               "slab-pipelined GPU decode overlapped with D2H into the pinned (Z,Y,X) uint32 volume"}
+                       "d2h_bytes_per_step": d2h, "seconds": e2e_s,
+                       "seconds_all": [round(x, 4) for x in times],
+                       "reduction": "best of 5 (host-timed, synchronised), max over ranks",
+                       "path": "decompress_volume(container, 0, out=pinned host array%s): H2D of directory+blobs, "
+                               "slab-pipelined GPU decode overlapped with D2H into the pinned (Z,Y,X) uint32 %s" %
+                               (", layers=this rank's bz range" if layers else "",
+                                "slab of each rank" if layers and world > 1 else "volume")}
+        e2e_check = check_bricks(blocks, pin, zr[0], brick_range[0], brick_range[1], grid)
+        line["e2e"]["check"] = e2e_check
         del pin
     if not args.no_cpu and not args.profile and rank == 0 and world == 1:
-        line["cpu_baseline"] = cpu_baseline(wl)
+        line["cpu_baseline"] = cpu_baselines(wl, cache_reqs)
     if rank == 0:
         print(json.dumps(line), flush=True)
 

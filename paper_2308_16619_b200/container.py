@@ -14,6 +14,7 @@ benchmark: compressed input already in HBM, output left in HBM.
 
 from __future__ import annotations
 
+import dataclasses
 import io
 import struct
 from dataclasses import dataclass, field
@@ -127,6 +128,21 @@ class CsvContainer:
         if len(data) != n:
             raise CorruptStreamError(f"detail section truncated for brick {index}")
         return np.frombuffer(data, dtype=np.uint8)
+
+    def with_detail_loaded(self) -> "CsvContainer":
+        """This container with its detail section in memory: ``self`` when it already
+        is, else a copy whose detail blob is read from the file of a cold open
+        (the bytes brick_detail() would read brick by brick, container.py:148-159)."""
+        if self.detail_blob is not None:
+            return self
+        size = int((self.directory["detail_off"].astype(np.int64) + self.directory["detail_bytes"]).max()) \
+            if self.directory.size else 0
+        with open(self._detail_file, "rb") as f:
+            f.seek(self._detail_base)
+            data = f.read(size)
+        if len(data) != size:
+            raise CorruptStreamError("detail section truncated")
+        return dataclasses.replace(self, detail_blob=np.frombuffer(data, dtype=np.uint8).copy())
 
     def detail_size(self, index: int) -> int:
         return int(self.directory[index]["detail_bytes"])
@@ -321,13 +337,17 @@ def _check_volume_results(vol, t, res):
 
 
 def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None = None, out: np.ndarray | None = None,
-                      slab_layers: int | None = None):
+                      slab_layers: int | None = None, layers: tuple[int, int] | None = None):
     """Reassemble the volume at LOD t, cropped to ceil(dims / 2**t) (container.py:456-478).
 
     ``workers`` is accepted for signature compatibility.  The decode runs on the
     GPU in slabs of whole bz layers, double-buffered so that each slab's
     device-to-host copy overlaps the next slab's decode.  ``out`` may be a
     preallocated (ideally pinned) uint32 host array of the cropped shape.
+    ``layers=(bz0, bz1)`` decodes only those brick layers (one rank's share of
+    a range-partitioned decode, distributed.rank_bricks): the result is that
+    z-slab, rows [bz0 * side, min(bz1 * side, cz)), and only its compressed
+    bytes are uploaded.
     """
     import torch
     from .device import GpuVolume
@@ -335,12 +355,21 @@ def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None =
     meta = container.meta
     x, y, z = meta.dims
     cz, cy, cx = (-(-d // (1 << t)) for d in (z, y, x))
+    gx, gy, gz = meta.grid_dims
+    side = meta.brick_side >> t
+    lz0, lz1 = layers if layers is not None else (0, gz)
+    if not 0 <= lz0 <= lz1 <= gz:
+        raise ValueError(f"layers {layers} outside [0, {gz}]")
+    rz0, rz1 = min(lz0 * side, cz), min(lz1 * side, cz)
     if out is None:
-        out = np.empty((cz, cy, cx), dtype=np.uint32)
-    elif out.shape != (cz, cy, cx) or out.dtype != np.uint32:
-        raise ValueError(f"out must be a uint32 array of shape {(cz, cy, cx)}")
+        out = np.empty((rz1 - rz0, cy, cx), dtype=np.uint32)
+    elif out.shape != (rz1 - rz0, cy, cx) or out.dtype != np.uint32:
+        raise ValueError(f"out must be a uint32 array of shape {(rz1 - rz0, cy, cx)}")
     if container.detail_blob is None:
-        raise ConfigError("device upload needs the detail section in memory")
+        if t > 0:   # levels above 0 never read the detail section (container.py:184-190)
+            container = dataclasses.replace(container, detail_blob=np.zeros(0, np.uint8))
+        else:
+            container = container.with_detail_loaded()
     # three-stage pipeline per slab of whole bz layers: upload its compressed
     # bytes (blobs are in brick order, container.py:428-445) -> decode -> D2H
     d = container.directory
@@ -356,15 +385,14 @@ def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None =
     try:
         n = vol.n_bricks
         dev = vol.device
-        gx, gy, gz = meta.grid_dims
-        side = meta.brick_side >> t
+        nl = lz1 - lz0
         if slab_layers is None:
-            slab_layers = max(1, -(-gz // 8))
+            slab_layers = max(1, -(-nl // 8))
         layer = gx * gy
         results = torch.empty((max(n, 1), 4), dtype=torch.int64, device=dev)
         host = torch.from_numpy(out.view(np.int32))
-        rows = min(slab_layers * side, cz)
-        bufs = [torch.empty((rows, cy, cx), dtype=torch.int32, device=dev) for _ in range(2 if gz > slab_layers else 1)]
+        rows = max(1, min(slab_layers * side, rz1 - rz0))
+        bufs = [torch.empty((rows, cy, cx), dtype=torch.int32, device=dev) for _ in range(2 if nl > slab_layers else 1)]
         comp = torch.cuda.current_stream(dev)
         up = torch.cuda.Stream(dev)
         # D2H of a slab split over 4 copy streams (one stream reaches ~44-48 GB/s, four ~50);
@@ -372,8 +400,13 @@ def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None =
         copies = [torch.cuda.Stream(dev) for _ in range(4)]
         freed = [[torch.cuda.Event() for _ in copies] for _ in bufs]
         ready = [torch.cuda.Event() for _ in bufs]
+        b_first = lz0 * layer
         uploaded = [0, 0, 0]
-        slabs = list(range(0, gz, slab_layers))
+        if b_first and n:   # a later rank: its blobs start at its first brick's offsets (brick order)
+            for k, (ocol, scale) in enumerate((("palette_off", 4), ("coarse_off", 1), ("detail_off", 1))):
+                uploaded[k] = min(int(d[ocol][b_first:min(lz1 * layer, n)].min()) * scale, blobs[k].size) \
+                    if lz1 > lz0 else 0
+        slabs = list(range(lz0, lz1, slab_layers))
 
         def upload_until(bz1):
             last = min(bz1 * layer, n) - 1
@@ -386,9 +419,9 @@ def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None =
             ev.record(up)
             return ev
 
-        up_ev = upload_until(min(slab_layers, gz))
+        up_ev = upload_until(min(lz0 + slab_layers, lz1))
         for k, bz0 in enumerate(slabs):
-            bz1 = min(bz0 + slab_layers, gz)
+            bz1 = min(bz0 + slab_layers, lz1)
             z0, z1 = min(bz0 * side, cz), min(bz1 * side, cz)
             i = k % len(bufs)
             comp.wait_event(up_ev)
@@ -403,16 +436,18 @@ def decompress_volume(container: CsvContainer, t: int = 0, workers: int | None =
                 if b > a:
                     cs.wait_event(ready[i])
                     with torch.cuda.stream(cs):
-                        host[a:b].copy_(bufs[i][a - z0: b - z0], non_blocking=True)
+                        host[a - rz0:b - rz0].copy_(bufs[i][a - z0: b - z0], non_blocking=True)
                 freed[i][h].record(cs)
             if k + 1 < len(slabs):
-                up_ev = upload_until(min(slabs[k + 1] + slab_layers, gz))
+                up_ev = upload_until(min(slabs[k + 1] + slab_layers, lz1))
         for s_ in copies:
             s_.synchronize()
         torch.cuda.synchronize(dev)
-        if t == meta.brick_log2 and n and bool((results[:n, 0] & 0xFFFFFFFF).eq(8).any()):
+        lo, hi = b_first, min(lz1 * layer, n)
+        res = results[lo:max(hi, lo)]
+        if t == meta.brick_log2 and hi > lo and bool((res[:, 0] & 0xFFFFFFFF).eq(8).any()):
             raise ValueError("expected 1 entries, got shape (0,)")   # morton_to_grid on an empty palette[:1]
-        GpuVolume.raise_first(results, n)
+        GpuVolume.raise_first(res, hi - lo)
     finally:
         vol.close()
     return out
@@ -433,7 +468,7 @@ def stats(container: CsvContainer) -> dict:
     n = meta.brick_count
     cn = d["coarse_nibbles"].astype(np.int64)
     dn = d["detail_nibbles"].astype(np.int64)
-    vol = container.to_device()
+    vol = container.with_detail_loaded().to_device()   # count mode reads every stream, detail included
     try:
         counts, sres = vol.op_counts()
     finally:

@@ -4,8 +4,26 @@ Bricks are independent (no cross-brick references), so rank r
 decodes bz layers [bz0, bz1) with no data-path collective: its palette,
 coarse and detail data are contiguous blob slices (brick-order blobs,
 container.py:428-445) and its output is the contiguous raster z-slab
-[bz0*side, min(bz1*side, Z)) x Y x X.  The only exchange is the optional
-final gather of the decoded slabs (NCCL all_gather over NVLink).
+[bz0*side, min(bz1*side, Z)) x Y x X.  The reference's thread pool over
+bricks (container.py:470-472) becomes this range partition over ranks.
+
+The only data exchange is the final gather of the decoded slabs:
+
+* ``gather="root"``: grouped point-to-point (``batch_isend_irecv`` =
+  ncclGroupStart / ncclSend / ncclRecv / ncclGroupEnd) straight into the
+  root's preallocated (Z, Y, X) volume -- each peer's slab lands in its own
+  contiguous z-row view, the root decodes its own slab in place, no padding
+  and no concatenation.
+* ``gather="all"``: every rank ends with the volume.  Equal slabs (the
+  2048^3 / 1024^3 workloads on 1, 2, 4, 8 ranks) use one
+  ``all_gather_into_tensor`` into the output itself; unequal ones one
+  broadcast per owner into its row view.
+
+Errors: every rank decodes without raising, then the ranks exchange their
+lowest failing global brick (status, stream, nibble) so that all ranks raise
+the same exception -- the one the reference raises for the lowest failing
+brick of the whole volume (container.py:470-478 walks bricks in order) --
+and nobody is left blocked in the gather.
 """
 
 from __future__ import annotations
@@ -13,6 +31,8 @@ from __future__ import annotations
 from typing import Callable
 
 import numpy as np
+
+NO_ERROR = np.iinfo(np.int64).max
 
 
 def bz_range(gz: int, world: int, rank: int) -> tuple[int, int]:
@@ -38,41 +58,138 @@ def rank_slab(dims: tuple[int, int, int], brick_log2: int, t: int, world: int, r
     return min(b0 * side, cz), min(b1 * side, cz)
 
 
-def decompress_volume_distributed(container, t: int = 0, group=None, gather: bool = True,
-                                  decode_slab: Callable | None = None):
-    """Decode this rank's slab; optionally all-gather the full cropped volume.
+def first_error(results, n: int, brick_begin: int, device=None):
+    """(global brick, status, stream, pos) of the lowest failing brick in a results
+    table (csv_result rows as int64[n, 4]), or (NO_ERROR, 0, 0, 0)."""
+    import torch
+    if n:
+        st = results[:n, 0] & 0xFFFFFFFF
+        bad = st.nonzero()
+        if bad.numel():
+            i = int(bad[0, 0])
+            from . import _lib
+            row = results[i].cpu().numpy().view(_lib.RESULT_DTYPE)[0]
+            return torch.tensor([brick_begin + i, int(row["status"]), int(row["stream"]), int(row["pos"])],
+                                dtype=torch.int64, device=device)
+    return torch.tensor([NO_ERROR, 0, 0, 0], dtype=torch.int64, device=device)
 
-    ``decode_slab(container, brick_range, z_range, t) -> (z1-z0, Y, X) tensor``
-    defaults to the GPU path (container.to_device + csv_decode_volume).  With
-    ``gather`` every rank returns the full volume (slabs exchanged with one
-    all_gather of equal-sized, zero-padded slabs); otherwise its own slab.
-    """
+
+def agree_on_error(err, group=None):
+    """All-gather every rank's (brick, status, stream, pos) and return the row of the
+    globally lowest failing brick (NO_ERROR if none): the same on every rank."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return err
+    allv = torch.empty((world, 4), dtype=torch.int64, device=err.device)
+    dist.all_gather_into_tensor(allv, err.reshape(1, 4).contiguous(), group=group)
+    return allv[int(torch.argmin(allv[:, 0]))]
+
+
+def raise_agreed(err) -> None:
+    brick, status, stream, pos = (int(v) for v in err.cpu().tolist())
+    if brick == NO_ERROR:
+        return
+    from .device import status_error
+    raise status_error(status, stream, pos)
+
+
+def gather_slabs(slab, out, dims, brick_log2: int, t: int, mode: str = "root", root: int = 0, group=None):
+    """Exchange decoded slabs.  ``slab`` is this rank's (z1-z0, cy, cx) rows (for the
+    root / every rank in "all" mode it may already be the view ``out[z0:z1]``);
+    ``out`` the (cz, cy, cx) volume on the receiving rank(s), None elsewhere."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    spans = [rank_slab(dims, brick_log2, t, world, r) for r in range(world)]
+    z0, z1 = spans[rank]
+    if mode == "root":
+        if rank == root:
+            if slab.data_ptr() != out[z0:z1].data_ptr():
+                out[z0:z1].copy_(slab)
+            ops = [dist.P2POp(dist.irecv, out[a:b], dist.get_global_rank(group, r) if group is not None else r,
+                              group=group)
+                   for r, (a, b) in enumerate(spans) if r != root and b > a]
+        else:
+            ops = [dist.P2POp(dist.isend, slab, dist.get_global_rank(group, root) if group is not None else root,
+                              group=group)] if z1 > z0 else []
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return out if rank == root else slab
+    if mode != "all":
+        raise ValueError(f"gather mode {mode!r} is not 'root' or 'all'")
+    if slab.data_ptr() != out[z0:z1].data_ptr():
+        out[z0:z1].copy_(slab)
+    rows = [b - a for a, b in spans]
+    if all(r == rows[0] for r in rows) and rows[0] * world == out.shape[0]:
+        # equal slabs: one collective writes every slab straight into place (the local one
+        # is its own input, an in-place all-gather)
+        dist.all_gather_into_tensor(out, out[z0:z1], group=group)
+    else:
+        for r, (a, b) in enumerate(spans):
+            if b > a:
+                dist.broadcast(out[a:b], dist.get_global_rank(group, r) if group is not None else r, group=group)
+    return out
+
+
+def decompress_volume_distributed(container, t: int = 0, group=None, gather: str | bool | None = "all",
+                                  root: int = 0, out=None, decode_slab: Callable | None = None):
+    """Decode this rank's whole-bz-layer slab and gather the cropped (Z, Y, X) volume.
+
+    ``container``: a CsvContainer (each rank uploads only its brick range).
+    ``gather``: "all" (every rank returns the volume), "root" (rank ``root``
+    returns it, the others their slab), None / False (each rank its slab).
+    ``out``: optional preallocated (cz, cy, cx) int32 tensor on the receiving
+    rank(s); the local slab is decoded straight into its rows.
+    ``decode_slab(container, brick_range, z_range, t) -> (err, slab)`` replaces
+    the GPU decode (CPU tests; ``err`` = int64[4] (global brick, status,
+    stream, pos) of the slab's lowest failing brick, brick NO_ERROR if none);
+    by default the slab is decoded by csv_decode_volume and the per-brick
+    statuses are checked collectively.
+    """
+    import torch
+    import torch.distributed as dist
+    if gather is True:
+        gather = "all"
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     meta = container.meta
-    grid = meta.grid_dims
-    b0, b1 = rank_bricks(grid, world, rank)
-    z0, z1 = rank_slab(meta.dims, meta.brick_log2, t, world, rank)
-    if decode_slab is None:
-        from .container import decompress_volume_device
-        vol = container.to_device(brick_range=(b0, b1))
-        slab = decompress_volume_device(vol, t, z_range=(z0, z1))
-    else:
-        slab = decode_slab(container, (b0, b1), (z0, z1), t)
-    if not gather or world == 1:
-        return slab
+    if not 0 <= t <= meta.brick_log2:
+        raise ValueError(f"LOD {t} outside [0, {meta.brick_log2}]")
     x, y, z = meta.dims
     cz, cy, cx = (-(-d // (1 << t)) for d in (z, y, x))
-    rows = max(rank_slab(meta.dims, meta.brick_log2, t, world, r)[1] - rank_slab(meta.dims, meta.brick_log2, t, world, r)[0]
-               for r in range(world))
-    pad = torch.zeros((rows, cy, cx), dtype=slab.dtype, device=slab.device)
-    pad[: slab.shape[0]] = slab
-    bufs = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(bufs, pad, group=group)
-    parts = []
-    for r in range(world):
-        s0, s1 = rank_slab(meta.dims, meta.brick_log2, t, world, r)
-        parts.append(bufs[r][: s1 - s0])
-    return torch.cat(parts, dim=0)
+    b0, b1 = rank_bricks(meta.grid_dims, world, rank)
+    z0, z1 = rank_slab(meta.dims, meta.brick_log2, t, world, rank)
+    receives = gather == "all" or (gather == "root" and rank == root) or world == 1
+    if decode_slab is None:
+        from . import _lib
+        _lib.require_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        if receives and out is None:
+            out = torch.empty((cz, cy, cx), dtype=torch.int32, device=dev)
+        vol = container.to_device(device=dev, brick_range=(b0, b1))
+        try:
+            slab, res = vol.decode(t, out=out[z0:z1] if receives else None, z_range=(z0, z1))
+            err = first_error(res, vol.n_bricks, b0, device=dev)
+            if t == meta.brick_log2 and vol.n_bricks and bool((res[:vol.n_bricks, 0] & 0xFFFFFFFF).eq(8).any()):
+                err = torch.tensor([b0, -1, 0, 0], dtype=torch.int64, device=dev)
+        finally:
+            vol.close()
+    else:
+        err, slab = decode_slab(container, (b0, b1), (z0, z1), t)
+        if receives and out is None:
+            out = torch.empty((cz, cy, cx), dtype=slab.dtype, device=slab.device)
+        if receives:
+            out[z0:z1].copy_(slab)
+            slab = out[z0:z1]
+    err = agree_on_error(err, group)
+    if int(err[1]) == -1:   # morton_to_grid on palette[:1] of an empty palette (coarsest LOD)
+        raise ValueError("expected 1 entries, got shape (0,)")
+    raise_agreed(err)
+    if world == 1:
+        return out if receives else slab
+    if not gather:
+        return slab
+    return gather_slabs(slab, out, meta.dims, meta.brick_log2, t, mode=gather, root=root, group=group)
