@@ -155,9 +155,12 @@ static int parse_head(const uint8_t* h, csv_volume* v, uint32_t* dtab_host) {
     v->V.X = d3[0]; v->V.Y = d3[1]; v->V.Z = d3[2];
     v->V.gx = v->grid[0]; v->V.gy = v->grid[1]; v->V.gz = v->grid[2];
     // packed decode tables {freq:16 | (slot-cum):12 | sym:4} (rans.py:31-62, codec.py:290-300)
+    v->V.fast_tab = 1;
     for (int tb = 0; tb < 2; ++tb) {
         uint16_t cnt[16];
         memcpy(cnt, h + 32 + 32 * tb, 32);
+        for (int s = 0; s < 16; ++s)
+            if (cnt[s] > 4095) v->V.fast_tab = 0;
         uint32_t sum = 0;
         for (int s = 0; s < 16; ++s) sum += cnt[s];
         if (sum != kTotalFreq && v->V.entropy) return fail(CSV_E_FORMAT, "counts must sum to 4096, got %u", sum);

@@ -389,6 +389,8 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_streams(VolView V, Plan P
     }
 }
 
+#include "csv_k1fast.cuh"
+
 // ============================================================================ K2: replay
 // Per-brick working set, sized for LMAX = N - t levels (compile-time):
 //   lev  : values of levels t+1..N in Morton order; level N-j at levoffA(j)
@@ -911,11 +913,38 @@ static void launch_k1_variant(const VolView& V, const Plan& P, unsigned long lon
     k1_streams<E, COUNT, MINB><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
 }
 
+template <int MINB>
+static void launch_k1f_variant(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, uint64_t blocks,
+                               cudaStream_t st) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        int b = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_fast<MINB>, K1_THREADS, 0) != cudaSuccess || b < 1)
+            b = MINB;
+        per_sm = b;
+    }
+    const uint64_t cap = (uint64_t)nsm * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    k1_fast<MINB><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
+}
+
+static bool k1_old() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("CSVGPU_K1"); v = (e && strcmp(e, "old") == 0) ? 1 : 0; }
+    return v == 1;
+}
+
 template <bool E, bool COUNT = false>
 static void launch_k1(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
     const uint64_t items = 2 * P.n;
     const uint64_t want = (items + 31) / 32;           // warps needed at one item per lane
     const uint64_t blocks = (want + K1_THREADS / 32 - 1) / (K1_THREADS / 32);
+    if (E && !COUNT && V.fast_tab && !k1_old()) {
+        if (blocks > (uint64_t)nsm * K1_MINB_LATENCY) launch_k1f_variant<K1_MINB_THROUGHPUT>(V, P, counter, nsm, blocks, st);
+        else launch_k1f_variant<K1_MINB_LATENCY>(V, P, counter, nsm, blocks, st);
+        return;
+    }
     if (blocks > (uint64_t)nsm * K1_MINB_LATENCY)      // more than one wave of the latency variant
         launch_k1_variant<E, COUNT, K1_MINB_THROUGHPUT>(V, P, counter, nsm, blocks, st);
     else

@@ -39,6 +39,7 @@ struct VolView {
     uint64_t brick_begin;
     uint64_t nb;
     uint32_t max_pal;          // longest palette (K2w works in u16 palette-index space)
+    int fast_tab;              // every table count <= 4095: K1f's packed table applies
 };
 
 constexpr uint32_t kWScratchStride = 4096;   // K2w scratch per warp slot (final-level parents, LMAX <= 5)
