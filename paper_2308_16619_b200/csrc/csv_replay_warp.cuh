@@ -29,6 +29,10 @@
 // inactive parents are written to HBM straight from the fill, the active ones
 // after their rounds.
 
+#ifndef K2W_SPAL
+#define K2W_SPAL 1      // u8 mode: copy the brick's palette into the warp's shared slice
+#endif
+
 namespace wk {
 
 __host__ __device__ constexpr uint32_t wofs(int j) {   // u16 offset of level N-j (root j = 0), 8-aligned
@@ -77,7 +81,7 @@ __host__ __device__ constexpr WLayout make_wlayout(int L, uint32_t isz) {
     }
     Y.cdesc = Y.clist + 2 * cpar;
     Y.spal = end;                                         // u8 mode: the brick's palette (<= 256 labels)
-    if (isz == 1) end = al16(end + 1024);
+    if (isz == 1 && K2W_SPAL) end = al16(end + 1024);
     Y.bytes = end;
     return Y;
 }
@@ -273,7 +277,7 @@ struct Brick {
 // label of a palette index (shared copy in u8 mode)
 template <typename IT>
 __device__ __forceinline__ uint32_t label_of(const Brick& B, uint32_t idx) {
-    return sizeof(IT) == 1 ? B.spal[idx] : __ldg(B.pal + idx);
+    return sizeof(IT) == 1 && K2W_SPAL ? B.spal[idx] : __ldg(B.pal + idx);
 }
 
 // raster voxel (x, y, z) of the brick at LOD t, nullptr if cropped (container.py:465-468)
@@ -289,7 +293,7 @@ __device__ __noinline__ void plane_rows_slow(Raster R, const Plan& P, const uint
                                              const IT* pl, uint32_t S2, uint32_t zz, int lane) {
     for (uint32_t e = lane; e < S2 * S2; e += 32) {
         uint32_t* const pp = raster_xyz(R, P, e % S2, e / S2, zz);
-        if (pp) *pp = sizeof(IT) == 1 ? spal[pl[e]] : __ldg(pal + pl[e]);
+        if (pp) *pp = sizeof(IT) == 1 && K2W_SPAL ? spal[pl[e]] : __ldg(pal + pl[e]);
     }
 }
 
@@ -697,7 +701,7 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         if (WIDE ? B.plen <= 256u : B.plen > 256u) continue;   // the other index width's pass
         B.out_m = MODE == OUT_MORTON ? P.out + P.dst[rr] : nullptr;
         B.pal = V.palette + V.pal_off[b];
-        if (sizeof(IT) == 1) {   // the palette (<= 256 labels) into the warp's slice
+        if (sizeof(IT) == 1 && K2W_SPAL) {   // the palette (<= 256 labels) into the warp's slice
             uint32_t* const sp = reinterpret_cast<uint32_t*>(base + Y.spal);
             for (uint32_t i = lane; i < B.plen; i += 32) sp[i] = __ldg(B.pal + i);
             B.spal = sp;
