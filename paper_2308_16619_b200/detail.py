@@ -166,17 +166,25 @@ class DeviceDetailStream(DetailStore):
         self._cap = 0
         self._host = None
         self._dev = None
+        self._dev_stream = None
         self.staged_bytes_total = 0
         self.staged_last_frame = 0
         self._ev = None
 
-    def _ensure(self, nbytes: int):
+    def _ensure(self, nbytes: int, stream):
+        """Grow the staging buffers.  The device buffer is allocated on, and its
+        predecessor released against, the stream the decodes that read it run
+        on (the caller's), so a decode still reading the old buffer keeps it alive."""
         torch = self._torch
         if nbytes > self._cap:
             cap = max(nbytes, 1 << 16)
             self._host = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
-            self._dev = torch.empty(cap + 64, dtype=torch.uint8, device=self.volume.device)
+            if self._dev is not None and self._dev_stream is not None:
+                self._dev.record_stream(self._dev_stream)
+            with torch.cuda.device(self.volume.device), torch.cuda.stream(stream):
+                self._dev = torch.empty(cap + 64, dtype=torch.uint8, device=self.volume.device)
             self._cap = cap
+        self._dev_stream = stream
 
     def stage(self, bricks, stream=None) -> None:
         """Make the level-0 streams of `bricks` readable by the next decode (take semantics)."""
@@ -196,13 +204,13 @@ class DeviceDetailStream(DetailStore):
         if len(streams) > 1:
             offs[1:] = np.cumsum(lens)[:-1]
         total = int(lens.sum())
-        self._ensure(max(total, 1))
+        dev = self.volume.device
+        stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        self._ensure(max(total, 1), stream)
         host = self._host.numpy()
         if total:
             np.concatenate(streams, out=host[:total])
-        dev = self.volume.device
-        with torch.cuda.device(dev), torch.cuda.stream(stream if stream is not None
-                                                      else torch.cuda.current_stream()):
+        with torch.cuda.device(dev), torch.cuda.stream(stream):
             # copy, index uploads, event and staging kernel all on the caller's stream
             if total:
                 self._dev[:total].copy_(self._host[:total], non_blocking=True)

@@ -46,6 +46,20 @@ def _ptr(a) -> int:
     return a.data_ptr()
 
 
+def _check_buffer(name: str, t, device, itemsize: int, shape=None, min_numel: int = 0) -> None:
+    """Refuse a caller buffer the kernels would index out of bounds: wrong device,
+    element size, a non-contiguous layout, a shape other than ``shape`` or fewer
+    than ``min_numel`` elements."""
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, the volume on {device}")
+    if t.element_size() != itemsize or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous tensor of {itemsize}-byte elements")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.numel() < min_numel:
+        raise ValueError(f"{name} has {t.numel()} elements, needs at least {min_numel}")
+
+
 def _stream_handle(torch, stream) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
@@ -183,6 +197,8 @@ class GpuVolume:
                 out = torch.empty((max(z1 - z0, 0), cy, cx), dtype=torch.int32, device=self.device)
             if results is None:
                 results = torch.empty((max(self.n_bricks, 1), 4), dtype=torch.int64, device=self.device)
+            _check_buffer("out", out, self.device, 4, shape=(max(z1 - z0, 0), cy, cx))
+            _check_buffer("results", results, self.device, 8, min_numel=4 * self.n_bricks)
             _lib.check(_lib.lib().csv_decode_volume(self._h, t, _ptr(out), z0, z1, _ptr(results),
                                                     _stream_handle(torch, stream)))
         return out, results
@@ -197,6 +213,9 @@ class GpuVolume:
     def decode_range(self, t: int, brick_first: int, brick_last: int, out, z_range, results, stream=None):
         """Raster decode of bricks [brick_first, brick_last) into the z-slab `out` (rows z_range)."""
         torch = self._torch
+        _, cy, cx = self.crop(t)
+        _check_buffer("out", out, self.device, 4, shape=(max(z_range[1] - z_range[0], 0), cy, cx))
+        _check_buffer("results", results, self.device, 8, min_numel=4 * max(brick_last - brick_first, 0))
         with _on_stream(torch, self.device, stream):
             _lib.check(_lib.lib().csv_decode_volume_range(self._h, t, brick_first, brick_last, _ptr(out),
                                                           z_range[0], z_range[1], _ptr(results),
@@ -210,6 +229,11 @@ class GpuVolume:
         with _on_stream(torch, self.device, stream):
             if results is None:
                 results = torch.empty((max(n, 1), 4), dtype=torch.int64, device=self.device)
+            for name, buf, size in (("lods", lods, 1), ("dst", dst, 8)):
+                _check_buffer(name, buf, self.device, size, min_numel=n)
+            _check_buffer("bricks", bricks, self.device, 4)
+            _check_buffer("pool", pool, self.device, 4)
+            _check_buffer("results", results, self.device, 8, min_numel=4 * n)
             _lib.check(_lib.lib().csv_decode_bricks(self._h, n, _ptr(bricks), _ptr(lods), _ptr(dst), _ptr(pool),
                                                     _ptr(results), _stream_handle(torch, stream)))
         return results

@@ -170,6 +170,52 @@ def test_stats_matches_reference(pkg, name):
     assert got == exp
 
 
+@pytest.mark.parametrize("name", ["d_b5_mem", "e_b4_raw"])
+def test_cold_container_stats_and_decode(pkg, name):
+    """A container opened with detail_cold=True (detail section left on disk,
+    container.py:148-159) gives the same stats() and the same volume at every LOD
+    as the hot one: the detail streams are read from the file, not taken as empty."""
+    import json
+    path = GOLDEN + f"/vol_{name}.csv1"
+    cold = pkg.CsvContainer.open(path, detail_cold=True)
+    assert cold.detail_blob is None
+    assert json.loads(json.dumps(pkg.stats(cold))) == golden_json("stats.json")[name]
+    g = golden_json(f"decode_{name}.json")
+    for t in range(g["brick_log2"] + 1):
+        assert h16(pkg.decompress_volume(cold, t)) == g["volume"][str(t)], t
+    assert cold.detail_blob is None          # the caller's container stays cold
+
+
+def test_device_buffers_validated(pkg):
+    """Caller-supplied device buffers of the wrong shape, dtype size, layout or
+    device are refused before any kernel could index past them."""
+    import torch
+    c = pkg.CsvContainer.from_bytes(golden_bytes("d_b5_mem"))
+    vol = c.to_device()
+    cz, cy, cx = vol.crop(0)
+    ok = torch.empty((cz, cy, cx), dtype=torch.int32, device="cuda")
+    vol.decode(0, out=ok)
+    for bad in (torch.empty((cz - 1, cy, cx), dtype=torch.int32, device="cuda"),
+                torch.empty((cz, cy, cx), dtype=torch.int16, device="cuda"),
+                torch.empty((cz, cx, cy), dtype=torch.int32, device="cuda").transpose(1, 2),
+                torch.empty((cz, cy, cx), dtype=torch.int32)):
+        with pytest.raises(ValueError):
+            vol.decode(0, out=bad)
+    with pytest.raises(ValueError, match="results"):
+        vol.decode(0, out=ok, results=torch.empty((1, 4), dtype=torch.int64, device="cuda"))
+    n = 4
+    bricks = torch.arange(n, dtype=torch.int32, device="cuda")
+    lods = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    dst = torch.arange(n, dtype=torch.int64, device="cuda") * (1 << 3 * c.meta.brick_log2)
+    pool = torch.empty(n << 3 * c.meta.brick_log2, dtype=torch.int32, device="cuda")
+    vol.decode_bricks(bricks, lods, dst, pool)
+    with pytest.raises(ValueError, match="dst"):
+        vol.decode_bricks(bricks, lods, dst.to(torch.int32), pool)
+    with pytest.raises(ValueError, match="lods"):
+        vol.decode_bricks(bricks, lods[:2], dst, pool)
+    vol.close()
+
+
 def test_stats_errors_match_rans_decode(pkg):
     """Corrupted streams raise rans_decode's messages (rans.py:192-197)."""
     with open(GOLDEN + "/vol_d_b5_mem.csv1", "rb") as f:

@@ -110,3 +110,21 @@ def test_cache_plan_matches_serial_semantics():
             for br, lod, start in live:
                 assert b.block_start[br] == start and b.resident_lod[br] == lod
             assert a.stats.decodes == b.stats.decodes
+
+
+def test_device_buffer_check():
+    """GpuVolume's guard on caller buffers (shape, element size, layout, device)."""
+    import torch
+    from paper_2308_16619_b200.device import _check_buffer
+    cpu = torch.device("cpu")
+    _check_buffer("out", torch.empty(2, 3, 4, dtype=torch.int32), cpu, 4, shape=(2, 3, 4))
+    with pytest.raises(ValueError, match="shape"):
+        _check_buffer("out", torch.empty(2, 3, 5, dtype=torch.int32), cpu, 4, shape=(2, 3, 4))
+    with pytest.raises(ValueError, match="contiguous"):
+        _check_buffer("out", torch.empty(2, 4, 3, dtype=torch.int32).transpose(1, 2), cpu, 4, shape=(2, 3, 4))
+    with pytest.raises(ValueError, match="contiguous"):
+        _check_buffer("out", torch.empty(2, 3, 4, dtype=torch.int64), cpu, 4, shape=(2, 3, 4))
+    with pytest.raises(ValueError, match="at least"):
+        _check_buffer("results", torch.empty(3, 4, dtype=torch.int64), cpu, 8, min_numel=16)
+    with pytest.raises(ValueError, match="is on"):
+        _check_buffer("out", torch.empty(1, dtype=torch.int32), torch.device("cuda", 0), 4)
