@@ -1048,7 +1048,7 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
     if (V.max_pal <= 65535u && !k2w_disabled()) {   // palette-index space: u8 pass, then u16 for long palettes
         if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint8_t>(Ls, V, P, counter + 1, nsm, st);
         else k2w_launch_mode<OUT_MORTON, uint8_t>(Ls, V, P, counter + 1, nsm, st);
-        if (V.max_pal > 256u) {
+        if (V.max_pal > e8::kMarkPal) {   // the u8 pass takes palettes of <= 253 labels (markers 253-255)
             if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint16_t>(Ls, V, P, counter + 2, nsm, st);
             else k2w_launch_mode<OUT_MORTON, uint16_t>(Ls, V, P, counter + 2, nsm, st);
         }

@@ -29,6 +29,8 @@
 // inactive parents are written to HBM straight from the fill, the active ones
 // after their rounds.
 
+#include "csv_eval8.cuh"
+
 #ifndef K2W_SPAL
 #define K2W_SPAL 1      // u8 mode: copy the brick's palette into the warp's shared slice
 #endif
@@ -49,9 +51,11 @@ __host__ __device__ constexpr uint32_t umax(uint32_t a, uint32_t b) { return a >
 //   ring  : final level: voxel planes 2pz-1, 2pz, 2pz+1 (3 x (2R)^2 values)
 //   plist : final level: per-plane active parents (u8 index in the plane)
 //   pdesc : final level: their pending-chain descriptors (u16); aliases cm
+//   amask : final level: active parents of the plane (bit per parent, raster
+//           order) + exclusive popcount per word (list index of a parent)
 //   clist/cdesc : coarse levels: active list / descriptors (u16); alias the ring
 struct WLayout {
-    uint32_t lev, pm, cm, wpre, ring, plist, pdesc, clist, cdesc, spal, bytes;   // byte offsets in one warp's slice
+    uint32_t lev, pm, cm, wpre, ring, plist, pdesc, clist, cdesc, spal, amask, bytes;   // byte offsets in one warp's slice
 };
 __host__ __device__ constexpr WLayout make_wlayout(int L, uint32_t isz) {
     WLayout Y{};
@@ -82,6 +86,8 @@ __host__ __device__ constexpr WLayout make_wlayout(int L, uint32_t isz) {
     Y.cdesc = Y.clist + 2 * cpar;
     Y.spal = end;                                         // u8 mode: the brick's palette (<= 256 labels)
     if (isz == 1 && K2W_SPAL) end = al16(end + 1024);
+    Y.amask = end;                                        // final level: per-plane active mask + word prefix (chain hops)
+    end = al16(end + 6 * ((R * R + 31) / 32));
     Y.bytes = end;
     return Y;
 }
@@ -257,6 +263,18 @@ __device__ __forceinline__ unsigned long long palette_children(uint64_t w, uint6
     return key;
 }
 
+// Exact first-error key of a failing group (the per-child restatement; only
+// runs when the SWAR evaluation flagged an error).
+__device__ __noinline__ unsigned long long exact_key(uint64_t w, uint32_t bf, int32_t ipq, uint32_t plen, uint32_t ent0,
+                                                     uint64_t vmask, bool leaf) {
+    Group g;
+    eval_group(w, 0u, 0u, 0u, 0u, bf, g);
+    const uint64_t pmk = m_pal(w);
+    unsigned long long pk = ~0ull;
+    if (pmk) pk = palette_children(w, pmk, ipq, plen, ent0, vmask, [](uint32_t, uint32_t) {});
+    return umin64(pk, group_errkey(ent0, w, vmask, leaf, g.bn));
+}
+
 struct Brick {
     uint64_t r;
     int N, t, n;
@@ -417,20 +435,29 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
             const uint32_t pxp = qx != Mx ? plev[morton_inc(q, Mx)] : 0u;
             const uint32_t pyp = qy != My ? plev[morton_inc(q, My)] : 0u;
             const uint32_t pzp = qz != Mz ? plev[morton_inc(q, Mz)] : 0u;
-            Group g;
-            eval_group(w, pv, pxp, pyp, pzp, bf, g);
-            store8<IT>(clev + 8 * q, g.v);
             cmb[q] = (uint8_t)(((~(w >> 3) & ONES) * 0x0102040810204080ull) >> 56);   // no stop: visited next level
-            pdesc[k] = (uint16_t)g.pend;
-            anyp |= g.pend;
-            const uint64_t pmk = m_pal(w);
-            unsigned long long pk = ~0ull;
-            if (pmk) {
-                pk = palette_children(w, pmk, ipq, B.plen, ent0, vmask,
-                                      [&](uint32_t c, uint32_t idx) { clev[8 * q + c] = (IT)idx; });
+            if constexpr (sizeof(IT) == 1) {
+                e8::Out g;
+                e8::eval8(w, pv, pxp, pyp, pzp, bf, ipq, B.plen, vmask, false, g);
+                *reinterpret_cast<uint2*>(clev + 8 * q) = make_uint2(g.vlo, g.vhi);
+                pdesc[k] = (uint16_t)g.pend;
+                anyp |= g.pend;
+                if (g.err) ek = umin64(ek, exact_key(w, bf, ipq, B.plen, ent0, vmask, false));
+            } else {
+                Group g;
+                eval_group(w, pv, pxp, pyp, pzp, bf, g);
+                store8<IT>(clev + 8 * q, g.v);
+                pdesc[k] = (uint16_t)g.pend;
+                anyp |= g.pend;
+                const uint64_t pmk = m_pal(w);
+                unsigned long long pk = ~0ull;
+                if (pmk) {
+                    pk = palette_children(w, pmk, ipq, B.plen, ent0, vmask,
+                                          [&](uint32_t c, uint32_t idx) { clev[8 * q + c] = (IT)idx; });
+                }
+                if (((m_op7(w) & vmask) != 0) | (g.bn != 0) | (pk != ~0ull))
+                    ek = umin64(ek, umin64(pk, group_errkey(ent0, w, vmask, false, g.bn)));
             }
-            if (((m_op7(w) & vmask) != 0) | (g.bn != 0) | (pk != ~0ull))
-                ek = umin64(ek, umin64(pk, group_errkey(ent0, w, vmask, false, g.bn)));
         }
     }
     __syncwarp();
@@ -461,16 +488,24 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
 }
 
 // ---------------------------------------------------------------- final level (plane sweep)
+// offset of child c (x, y bits) of plane parent i = px + RR * py inside a ring voxel plane
+template <int RR>
+__device__ __forceinline__ uint32_t child_off(uint32_t i, uint32_t c) {
+    return (2 * (i / RR) + ((c >> 1) & 1u)) * (2 * RR) + 2 * (i % RR) + (c & 1u);
+}
+
 // Ring voxel plane z (u16, (2R)^2) at ring + (z % 3) * (2R)^2; child (cx, cy) at cy * 2R + cx.
 template <int MODE, int RR, typename IT>
 __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const Plan& P, const IT* plev,
                                                          const uint32_t* pm, uint16_t* wpre, IT* ring,
-                                                         uint8_t* plist, uint16_t* pdesc, uint32_t& cur,
-                                                         uint32_t& ip_run, uint32_t& pdl, int lane) {
+                                                         uint8_t* plist, uint16_t* pdesc, uint32_t* amask,
+                                                         uint32_t& cur, uint32_t& ip_run, uint32_t& pdl, int lane) {
     constexpr uint32_t Pn = RR * RR * RR, W = (Pn + 31) / 32;
     constexpr uint32_t PP = RR * RR;                    // parents per plane
     constexpr uint32_t S2 = 2 * RR;                     // children per row
     constexpr uint32_t PL = S2 * S2;                    // u16 per voxel plane
+    constexpr uint32_t AW = (PP + 31) / 32;             // active-mask words per plane
+    uint16_t* const apre = reinterpret_cast<uint16_t*>(amask + AW);
     const bool leaf = B.t == 0;
     const uint32_t nact = rank_prefix(pm, W, wpre, lane);
     const uint8_t* const E = leaf ? B.Ed : B.Ec;
@@ -514,14 +549,20 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
             if (ok) {
                 pv = plev[q];
                 mw = pm[q >> 5];
+            }
+            const bool act = ok && ((mw >> (q & 31)) & 1u);
+            if (ok && !act) {   // active parents' children are all written by the active pass
                 const P2 pp = pack2<IT>(pv, pv);
                 r0[(2 * py) * RR + px] = pp;
                 r0[(2 * py + 1) * RR + px] = pp;
                 r1[(2 * py) * RR + px] = pp;
                 r1[(2 * py + 1) * RR + px] = pp;
             }
-            const bool act = ok && ((mw >> (q & 31)) & 1u);
             const uint32_t bal = __ballot_sync(FULL, act);
+            if (lane == 0 && i0 < PP) {
+                amask[i0 >> 5] = bal;
+                apre[i0 >> 5] = (uint16_t)nl;
+            }
             if (act) {
                 plist[nl + __popc(bal & lanemask_lt(lane))] = (uint8_t)i;
             } else if (MODE == OUT_MORTON && ok) {
@@ -545,13 +586,28 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
                 const uint32_t ent0 = e0 + 8 * rank;
                 const uint64_t w = ent0 + 8 <= cap ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
                 const uint64_t vmask = valid_mask(nvalid, ent0);
-                pdl += __popcll(m_op5(w) & vmask);
                 const uint32_t pv = plev[q];
                 const uint32_t bf = (px == 0) | ((px == RR - 1) << 1) | ((py == 0) << 2) | ((py == RR - 1) << 3) |
                                     ((pz == 0) << 4) | ((pz == RR - 1) << 5);
                 const uint32_t pxp = px + 1 < RR ? plev[spread3_u32(px + 1) | sy | sz] : 0u;
                 const uint32_t pyp = py + 1 < RR ? plev[sx | (spread3_u32(py + 1) << 1) | sz] : 0u;
                 const uint32_t pzp = pz + 1 < RR ? plev[sx | sy | (spread3_u32(pz + 1) << 2)] : 0u;
+                if constexpr (sizeof(IT) == 1) {
+                    // palette base only when the group has palette ops (op bit 2)
+                    const int32_t ipq = (w & 0x0404040404040404ull) ? (int32_t)B.ipb[rank] : 0;
+                    e8::Out g;
+                    e8::eval8(w, pv, pxp, pyp, pzp, bf, ipq, B.plen, vmask, leaf, g);
+                    pdl += g.n5;
+                    r0[(2 * py) * RR + px] = (P2)(g.vlo & 0xFFFFu);
+                    r0[(2 * py + 1) * RR + px] = (P2)(g.vlo >> 16);
+                    r1[(2 * py) * RR + px] = (P2)(g.vhi & 0xFFFFu);
+                    r1[(2 * py + 1) * RR + px] = (P2)(g.vhi >> 16);
+                    pdesc[k] = (uint16_t)g.pend;
+                    anyp |= g.pend;
+                    if (g.err) ek = umin64(ek, exact_key(w, bf, ipq, B.plen, ent0, vmask, leaf));
+                    continue;
+                }
+                pdl += __popcll(m_op5(w) & vmask);
                 Group g;
                 eval_group(w, pv, pxp, pyp, pzp, bf, g);
                 r0[(2 * py) * RR + px] = pack2<IT>(g.v[0], g.v[1]);
@@ -580,30 +636,38 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
         const IT* const pr = ring + ((2 * pz + 2) % 3) * PL;   // voxel plane 2pz-1
         IT* const p0 = ring + ((2 * pz) % 3) * PL;
         IT* const p1 = ring + ((2 * pz + 1) % 3) * PL;
-        // ---- chain rounds: child c <- child c | (1 << axis) of the -1 neighbour (ring)
+        // ---- pending chains: child c of an active parent copies child c | (1 << axis) of
+        // the -1 neighbour parent (codec.py:422-423); that child is final unless it is
+        // itself pending (one more odd coordinate, so at most three hops), or lies in the
+        // previous voxel plane (z), which is final.  One pass, no rounds.
         if (__any_sync(FULL, anyp != 0u)) {
 #pragma unroll 1
-            for (int rd = 0; rd < 3; ++rd) {
-                const uint32_t cls = rd == 0 ? kClass1 : (rd == 1 ? kClass2 : kClass3);
+            for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                uint32_t d = k < nl ? (uint32_t)pdesc[k] : 0u;
+                if (!__any_sync(FULL, d != 0u)) continue;
+                const uint32_t i = d ? plist[k] : 0u;
+                while (d) {
+                    const uint32_t c = (uint32_t)(__ffs(d) - 1) >> 1;
+                    uint32_t a = (d >> (2 * c)) & 3u;
+                    d &= ~(3u << (2 * c));
+                    uint32_t ii = i, cc = c;
+                    const IT* src;
 #pragma unroll 1
-                for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
-                    const uint32_t k = k0 + lane;
-                    uint32_t m = k < nl ? (uint32_t)pdesc[k] & cls : 0u;
-                    if (!__any_sync(FULL, m != 0u)) continue;
-                    const uint32_t i = m ? plist[k] : 0u;
-                    const uint32_t cx0 = 2 * (i % RR), cy0 = 2 * (i / RR);
-                    while (m) {
-                        const uint32_t c = (uint32_t)(__ffs(m) - 1) >> 1;
-                        const uint32_t a1 = (m >> (2 * c)) & 3u;
-                        m &= ~(3u << (2 * c));
-                        const uint32_t cx = cx0 + (c & 1), cy = cy0 + ((c >> 1) & 1);
-                        IT* const dst = ((c & 4) ? p1 : p0) + cy * S2 + cx;
-                        const IT* const src = a1 == 1u ? dst - 1 : (a1 == 2u ? dst - S2 : ((c & 4) ? p0 : pr) + cy * S2 + cx);
-                        *dst = *src;
+                    for (;;) {
+                        cc |= 1u << (a - 1u);
+                        if (a == 3u) { src = pr + child_off<RR>(ii, cc); break; }
+                        ii -= a == 1u ? 1u : RR;
+                        const uint32_t wd = amask[ii >> 5], bit = 1u << (ii & 31);
+                        uint32_t a2 = 0;
+                        if (wd & bit) a2 = ((uint32_t)pdesc[apre[ii >> 5] + __popc(wd & (bit - 1u))] >> (2 * cc)) & 3u;
+                        if (a2 == 0u) { src = ((cc & 4) ? p1 : p0) + child_off<RR>(ii, cc); break; }
+                        a = a2;
                     }
+                    (((c & 4) ? p1 : p0) + child_off<RR>(i, c))[0] = *src;
                 }
-                __syncwarp();
             }
+            __syncwarp();
         }
         if (MODE == OUT_RASTER) {
             // ---- the plane pair to HBM as whole rows (each sector written once)
@@ -656,6 +720,201 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
     return warp_min64(ek);
 }
 
+// ---------------------------------------------------------------- final level, u8 (marker chains)
+// The u8 pass (palettes of <= 253 labels, indices <= 252) leaves every pending
+// child as the marker byte 252 + axis (e8::eval8<true>) and resolves the chains
+// word by word over the ring rows instead of per child:
+//   * a pending child copies the -1 neighbour on its axis (codec.py:422-423);
+//     x-pending children sit at even x, y at even y, z at even z;
+//   * odd rows have no y markers, and their x markers' sources (odd x) are
+//     final once the z markers are: phase 0 resolves odd rows (z from the
+//     previous voxel plane, then x from the byte to the left, a byte_perm with
+//     the left lane's word);
+//   * phase 1 resolves even rows: z, y from the already resolved odd row
+//     above, then x.
+// Resolution is fused with the whole-row raster write (each 16-byte row chunk
+// is resolved, written back for later readers and stored as labels).
+template <int MODE, int RR>
+__device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const Plan& P, const uint8_t* plev,
+                                                          const uint32_t* pm, uint16_t* wpre, uint8_t* ring,
+                                                          uint8_t* plist, uint32_t& cur, uint32_t& ip_run,
+                                                          uint32_t& pdl, int lane) {
+    static_assert(RR >= 4, "word-wise rows need >= 8 children per row");
+    constexpr uint32_t Pn = RR * RR * RR, W = (Pn + 31) / 32;
+    constexpr uint32_t PP = RR * RR;           // parents per plane
+    constexpr uint32_t S2 = 2 * RR;            // children (bytes) per row
+    constexpr uint32_t PL = S2 * S2;           // bytes per voxel plane
+    constexpr uint32_t WPR = S2 / 4;           // words per row
+    constexpr uint32_t HW = PP / 2;            // words in the rows of one parity
+    constexpr uint32_t LG = RR == 4 ? 2 : (RR == 8 ? 3 : 4);
+    constexpr uint32_t MX = 0x49249u & ((1u << (3 * LG)) - 1u), MY = MX << 1, MZ = MX << 2;
+    const bool leaf = B.t == 0;
+    const uint32_t nact = rank_prefix(pm, W, wpre, lane);
+    const uint8_t* const E = leaf ? B.Ed : B.Ec;
+    const uint32_t cap = leaf ? B.capd : B.capc;
+    const uint32_t nvalid = leaf ? B.srd.n_entries : B.src.n_entries;
+    const uint32_t e0 = cur;
+    unsigned long long ek = ~0ull;
+    if ((uint64_t)e0 + 8ull * nact > nvalid) ek = ekey(nvalid, 0, EK_UNDERRUN_NV);
+    {   // palette base per active parent, in entry (rank) order (codec.py:453-457) -> per-warp scratch
+        auto ld = [&](uint32_t k) -> uint64_t {
+            const uint32_t ent0 = e0 + 8 * k;
+            return (k < nact && ent0 + 8 <= cap) ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+        };
+        uint64_t wn = ld(lane), wnn = ld(32 + lane);
+        for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const uint64_t w = wn;
+            wn = wnn;
+            wnn = ld(k0 + 64 + lane);
+            const uint32_t c6 = __popcll(m_op6(w)), inc6 = warp_incl(c6, lane);
+            if (k < nact) B.ipb[k] = (uint16_t)(ip_run + inc6 - c6);
+            ip_run += __shfl_sync(FULL, inc6, 31);
+        }
+    }
+    __syncwarp();
+    const bool fast = MODE == OUT_RASTER && B.al16r;
+#pragma unroll 1
+    for (uint32_t pz = 0; pz < RR; ++pz) {
+        const uint32_t sz = spread3_u32(pz) << 2;
+        uint8_t* const r0 = ring + ((2 * pz) % 3) * PL;         // voxel plane 2pz
+        uint8_t* const r1 = ring + ((2 * pz + 1) % 3) * PL;     // voxel plane 2pz+1
+        const uint8_t* const pr = ring + ((2 * pz + 2) % 3) * PL;   // voxel plane 2pz-1 (final)
+        uint16_t* const h0 = reinterpret_cast<uint16_t*>(r0);
+        uint16_t* const h1 = reinterpret_cast<uint16_t*>(r1);
+        // ---- fill: inactive parents' children = the parent value (ring; Morton: HBM); active list
+        uint32_t nl = 0;
+#pragma unroll
+        for (uint32_t i0 = 0; i0 < PP; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool ok = i < PP;
+            const uint32_t px = i % RR, py = i / RR;
+            const uint32_t q = spread3_u32(px) | (spread3_u32(py) << 1) | sz;
+            uint32_t mw = 0, pv = 0;
+            if (ok) {
+                pv = plev[q];
+                mw = pm[q >> 5];
+            }
+            const bool act = ok && ((mw >> (q & 31)) & 1u);
+            if (ok && !act) {
+                const uint16_t pp = (uint16_t)(pv * 0x0101u);
+                h0[(2 * py) * RR + px] = pp;
+                h0[(2 * py + 1) * RR + px] = pp;
+                h1[(2 * py) * RR + px] = pp;
+                h1[(2 * py + 1) * RR + px] = pp;
+                if (MODE == OUT_MORTON) {
+                    const uint32_t l = label_of<uint8_t>(B, pv);
+                    const uint32_t lab[8] = {l, l, l, l, l, l, l, l};
+                    store_children<MODE>(B, P, q, px, py, pz, lab);
+                }
+            }
+            const uint32_t bal = __ballot_sync(FULL, act);
+            if (act) plist[nl + __popc(bal & lanemask_lt(lane))] = (uint8_t)i;
+            nl += __popc(bal);
+        }
+        __syncwarp();
+        // ---- active parents: one lane each, SWAR evaluation, pending children as markers
+        for (uint32_t k0 = 0; k0 < nl; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            if (k < nl) {
+                const uint32_t i = plist[k];
+                const uint32_t px = i % RR, py = i / RR;
+                const uint32_t q = spread3_u32(px) | (spread3_u32(py) << 1) | sz;
+                const uint32_t rank = wpre[q >> 5] + __popc(pm[q >> 5] & ((1u << (q & 31)) - 1u));
+                const uint32_t ent0 = e0 + 8 * rank;
+                const uint64_t w = ent0 + 8 <= cap ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+                const uint64_t vmask = valid_mask(nvalid, ent0);
+                const uint32_t pv = plev[q];
+                const uint32_t bf = (px == 0) | ((px == RR - 1) << 1) | ((py == 0) << 2) | ((py == RR - 1) << 3) |
+                                    ((pz == 0) << 4) | ((pz == RR - 1) << 5);
+                // +1 neighbours (wrap around at the maximum: value unused, BAD_NEIGHBOR)
+                const uint32_t pxp = plev[morton_inc(q, MX)];
+                const uint32_t pyp = plev[morton_inc(q, MY)];
+                const uint32_t pzp = plev[morton_inc(q, MZ)];
+                const int32_t ipq = (w & 0x0404040404040404ull) ? (int32_t)B.ipb[rank] : 0;   // palette ops only
+                e8::Out g;
+                e8::eval8<true>(w, pv, pxp, pyp, pzp, bf, ipq, B.plen, vmask, leaf, g);
+                pdl += g.n5;
+                h0[(2 * py) * RR + px] = (uint16_t)g.vlo;
+                h0[(2 * py + 1) * RR + px] = (uint16_t)(g.vlo >> 16);
+                h1[(2 * py) * RR + px] = (uint16_t)g.vhi;
+                h1[(2 * py + 1) * RR + px] = (uint16_t)(g.vhi >> 16);
+                if (g.err) ek = umin64(ek, exact_key(w, bf, ipq, B.plen, ent0, vmask, leaf));
+            }
+        }
+        __syncwarp();
+        // ---- marker chains, row parity by row parity; fast raster: resolve + write whole rows
+#pragma unroll 1
+        for (int dz = 0; dz < 2; ++dz) {
+            uint8_t* const pl = dz ? r1 : r0;
+            uint32_t* const zb = fast ? B.R.base + (2 * pz + dz) * B.plane : nullptr;
+#pragma unroll 1
+            for (int ph = 0; ph < 2; ++ph) {
+#pragma unroll
+                for (uint32_t w0 = 0; w0 < HW; w0 += 32) {
+                    const uint32_t wi = w0 + lane;
+                    const bool okw = wi < HW;
+                    const uint32_t row = 2 * (wi / WPR) + (ph ? 0u : 1u), cw = wi % WPR;
+                    uint32_t* const wp = reinterpret_cast<uint32_t*>(pl + row * S2) + cw;
+                    const uint32_t x = okw ? *wp : 0u;
+                    const uint32_t f = ((x & 0x7F7F7F7Fu) + 0x03030303u) & x & 0x80808080u;   // bytes >= 253
+                    const uint32_t a0 = x << 7, a1 = x << 6;                                 // axis bits at bit 7
+                    uint32_t y = x;
+                    if (f) {
+                        const uint32_t mz = dz == 0 ? f & a0 & a1 : 0u;
+                        if (mz) {
+                            const uint32_t M = (mz >> 7) * 0xFFu;
+                            y = (y & ~M) | (*reinterpret_cast<const uint32_t*>(pr + row * S2 + 4 * cw) & M);
+                        }
+                        const uint32_t my = ph ? f & ~a0 & a1 : 0u;
+                        if (my) {
+                            const uint32_t M = (my >> 7) * 0xFFu;
+                            y = (y & ~M) | (*(wp - WPR) & M);
+                        }
+                    }
+                    const uint32_t left = __shfl_up_sync(FULL, y, 1);
+                    const uint32_t mx = f & a0 & ~a1;
+                    if (mx) {
+                        const uint32_t M = (mx >> 7) * 0xFFu;
+                        y = (y & ~M) | (__byte_perm(y, left, 0x2107) & M);
+                    }
+                    if (f) *wp = y;
+                    if (fast && okw) {
+                        const uint4 lab = make_uint4(label_of<uint8_t>(B, y & 0xFFu), label_of<uint8_t>(B, (y >> 8) & 0xFFu), label_of<uint8_t>(B, (y >> 16) & 0xFFu),
+                                                     label_of<uint8_t>(B, y >> 24));
+                        __stcs(reinterpret_cast<uint4*>(zb + row * B.pitch + 4 * cw), lab);   // evict-first
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (!fast) {
+            if (MODE == OUT_RASTER) {
+#pragma unroll 1
+                for (int dz = 0; dz < 2; ++dz)
+                    plane_rows_slow<uint8_t>(B.R, P, B.spal, B.pal, dz ? r1 : r0, S2, 2 * pz + dz, lane);
+            } else {
+                for (uint32_t k0 = 0; k0 < nl; k0 += 32) {   // active parents to HBM (8 children = one sector)
+                    const uint32_t k = k0 + lane;
+                    if (k < nl) {
+                        const uint32_t i = plist[k];
+                        const uint32_t px = i % RR, py = i / RR;
+                        const uint32_t q = spread3_u32(px) | (spread3_u32(py) << 1) | sz;
+                        const uint32_t a = h0[(2 * py) * RR + px], b = h0[(2 * py + 1) * RR + px];
+                        const uint32_t c = h1[(2 * py) * RR + px], d = h1[(2 * py + 1) * RR + px];
+                        const uint32_t lab[8] = {label_of<uint8_t>(B, a & 0xFFu), label_of<uint8_t>(B, a >> 8), label_of<uint8_t>(B, b & 0xFFu), label_of<uint8_t>(B, b >> 8),
+                                                 label_of<uint8_t>(B, c & 0xFFu), label_of<uint8_t>(B, c >> 8), label_of<uint8_t>(B, d & 0xFFu), label_of<uint8_t>(B, d >> 8)};
+                        store_children<MODE>(B, P, q, px, py, pz, lab);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    cur = e0 + 8 * nact;
+    return warp_min64(ek);
+}
+
 }  // namespace wk
 
 #ifndef K2W_MINB
@@ -682,6 +941,7 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
     uint16_t* const pdesc = reinterpret_cast<uint16_t*>(base + Y.pdesc);
     uint16_t* const clist = reinterpret_cast<uint16_t*>(base + Y.clist);
     uint16_t* const cdesc = reinterpret_cast<uint16_t*>(base + Y.cdesc);
+    uint32_t* const amask = reinterpret_cast<uint32_t*>(base + Y.amask);
     const int lane = threadIdx.x & 31;
     while (true) {
         __syncwarp();
@@ -698,7 +958,7 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         B.n = B.N - B.t;
         if (B.t < B.N && B.n > LMAX) continue;          // served by the global-workspace kernel
         B.plen = V.pal_len[b];
-        if (WIDE ? B.plen <= 256u : B.plen > 256u) continue;   // the other index width's pass
+        if (WIDE ? B.plen <= e8::kMarkPal : B.plen > e8::kMarkPal) continue;   // the other index width's pass
         B.out_m = MODE == OUT_MORTON ? P.out + P.dst[rr] : nullptr;
         B.pal = V.palette + V.pal_off[b];
         if (sizeof(IT) == 1 && K2W_SPAL) {   // the palette (<= 256 labels) into the warp's slice
@@ -773,12 +1033,22 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         uint32_t& cur = B.t == 0 ? cur_d : cur_c;
         uint32_t& pdl = B.t == 0 ? pdd : pdc;
         unsigned long long ek;
-        switch (B.n) {
-            case 1: ek = final_sweep<MODE, 1, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
-            case 2: ek = final_sweep<MODE, 2, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
-            case 3: ek = final_sweep<MODE, 4, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
-            case 4: ek = final_sweep<MODE, (LMAX >= 4 ? 8 : 1), IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
-            default: ek = final_sweep<MODE, (LMAX >= 5 ? 16 : 1), IT>(B, P, plev, pm, wpre, ring, plist, fdesc, cur, ip_run, pdl, lane); break;
+        if constexpr (sizeof(IT) == 1) {
+            switch (B.n) {
+                case 1: ek = final_sweep<MODE, 1, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 2: ek = final_sweep<MODE, 2, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 3: ek = final_sweep8<MODE, 4>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+                case 4: ek = final_sweep8<MODE, (LMAX >= 4 ? 8 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+                default: ek = final_sweep8<MODE, (LMAX >= 5 ? 16 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+            }
+        } else {
+            switch (B.n) {
+                case 1: ek = final_sweep<MODE, 1, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 2: ek = final_sweep<MODE, 2, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 3: ek = final_sweep<MODE, 4, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 4: ek = final_sweep<MODE, (LMAX >= 4 ? 8 : 1), IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                default: ek = final_sweep<MODE, (LMAX >= 5 ? 16 : 1), IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+            }
         }
         if (ek != ~0ull) {
             if (B.t == 0) report_error(P, rr, B.Ed, B.capd, B.srd, ek, true, lane);

@@ -214,7 +214,9 @@ class GpuVolume:
         """Raster decode of bricks [brick_first, brick_last) into the z-slab `out` (rows z_range)."""
         torch = self._torch
         _, cy, cx = self.crop(t)
-        _check_buffer("out", out, self.device, 4, shape=(max(z_range[1] - z_range[0], 0), cy, cx))
+        _check_buffer("out", out, self.device, 4, min_numel=max(z_range[1] - z_range[0], 0) * cy * cx)
+        if out.dim() != 3 or tuple(out.shape[1:]) != (cy, cx):
+            raise ValueError(f"out has shape {tuple(out.shape)}, expected (>= {z_range[1] - z_range[0]}, {cy}, {cx})")
         _check_buffer("results", results, self.device, 8, min_numel=4 * max(brick_last - brick_first, 0))
         with _on_stream(torch, self.device, stream):
             _lib.check(_lib.lib().csv_decode_volume_range(self._h, t, brick_first, brick_last, _ptr(out),

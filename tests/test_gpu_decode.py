@@ -267,6 +267,50 @@ def test_mixed_palette_widths(pkg, oracle):
         assert np.array_equal(host[dst[k]: dst[k] + sizes[k]], ref), (i, t)
 
 
+def test_palette_width_boundaries(pkg, oracle):
+    """Bricks whose palettes straddle the u8 pass's limit (<= 253 labels: indices
+    0-252, bytes 253-255 mark pending neighbour chains) and the u8/u16 split:
+    blocky bricks with exactly P labels each (many neighbour ops, P = 1 .. 300),
+    plus 1-voxel membranes, every LOD, raster and Morton, against the oracle."""
+    import torch
+    b = 32
+    zz, yy, xx = np.meshgrid(np.arange(b), np.arange(b), np.arange(b), indexing="ij")
+
+    def brick(s_, P, per):   # blocks of s_^3 voxels over P labels, optional 1-voxel planes of label 0
+        lab = ((xx // s_) + 16 * (yy // s_) + 256 * (zz // s_)) * 7919 % P
+        return np.where((xx + 2 * yy + zz) % per == 0, 0, lab) if per else lab
+
+    # (block, labels, plane period) -> palette length 250 .. 258 (searched with the oracle encoder)
+    specs = [(6, 69, 7), (6, 81, 0), (6, 81, 7), (6, 93, 7), (6, 234, 0), (6, 87, 0), (6, 87, 7), (5, 60, 11),
+             (6, 159, 7), (4, 9, 0), (8, 3, 5), (6, 40, 7)]
+    vol = np.zeros((b, 2 * b, 6 * b), dtype=np.uint32)                  # (Z, Y, X): 12 bricks
+    for k, sp in enumerate(specs):
+        by, bx = divmod(k, 6)
+        vol[:, by * b:(by + 1) * b, bx * b:(bx + 1) * b] = brick(*sp) + 1000 * k
+    oc = oracle.compress_volume(vol, brick_log2=5)
+    pal = sorted(set(int(v) for v in oc.directory[:, 1]))
+    assert set(range(250, 259)) <= set(pal), pal
+    c = pkg.CsvContainer.from_bytes(oc.to_bytes())
+    for t in range(6):
+        bad, _, ref = oracle.decompress_volume(oc, t)
+        assert bad == -1
+        assert np.array_equal(pkg.decompress_volume(c, t), ref), t
+    v = c.to_device()
+    n = oc.n_bricks
+    reqs = [(i, t) for i in range(n) for t in (0, 1, 2, 3)]
+    sizes = [8 ** (5 - t) for _, t in reqs]
+    dst = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    pool = torch.zeros(int(sum(sizes)), dtype=torch.int32, device="cuda")
+    res = v.decode_bricks(torch.tensor([r[0] for r in reqs], dtype=torch.int32, device="cuda"),
+                          torch.tensor([r[1] for r in reqs], dtype=torch.uint8, device="cuda"),
+                          torch.from_numpy(dst).cuda(), pool)
+    pkg.GpuVolume.raise_first(res, len(reqs))
+    host = pool.cpu().numpy().view(np.uint32)
+    for k, (i, t) in enumerate(reqs):
+        _, ref = oracle.container_decode_brick(oc, i, t)
+        assert np.array_equal(host[dst[k]: dst[k] + sizes[k]], ref), (i, t)
+
+
 def test_cta_fallback_kernel(tmp_path):
     """The CTA-per-brick replay (k2_fast) still serves palettes > 65535 entries; force it
     for a whole process (CSVGPU_K2=cta) and check goldens at every LOD, raster and Morton."""
