@@ -31,6 +31,14 @@
 
 #include "csv_eval8.cuh"
 
+#ifndef K2W_RUNROLL
+#define K2W_RUNROLL 1   // u8 final level: unroll of the per-plane row loop
+#endif
+#ifndef K2W_RBRANCH
+#define K2W_RBRANCH 0   // u8 final level: branch around the z / y marker steps (0: predicated, faster)
+#endif
+constexpr int kRUnroll = K2W_RUNROLL;
+
 #ifndef K2W_SPAL
 #define K2W_SPAL 1      // u8 mode: copy the brick's palette into the warp's shared slice
 #endif
@@ -720,6 +728,59 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
     return warp_min64(ek);
 }
 
+// One voxel plane's rows of one parity: resolve the chain markers word by word
+// (4 children per lane), write the words back where later phases / the next
+// plane read them, and (fast raster) store the labels as whole 16-byte rows.
+//   DZ = 0: even voxel plane 2pz (z markers from the previous plane `pr`),
+//   PH = 0: odd rows (no y markers), PH = 1: even rows (y from the odd row above).
+template <int RR, int DZ, int PH>
+__device__ __forceinline__ void resolve_rows(const Brick& B, uint8_t* pl, const uint8_t* pr, bool fast, uint32_t* zb,
+                                             int lane) {
+    static_assert(K2W_SPAL, "the u8 pass reads labels from the shared palette copy");
+    constexpr uint32_t S2 = 2 * RR, WPR = S2 / 4, HW = RR * RR / 2, RPI = 32 / WPR;   // row pairs per iteration
+    const uint32_t rp0 = lane / WPR, cw = lane % WPR;
+    const uint32_t row0 = 2 * rp0 + (PH ? 0u : 1u);
+    uint32_t* wp = reinterpret_cast<uint32_t*>(pl + row0 * S2) + cw;
+    const uint32_t* pw = reinterpret_cast<const uint32_t*>(pr + row0 * S2) + cw;
+    uint32_t* op = fast ? zb + row0 * B.pitch + 4 * cw : nullptr;
+    const uint8_t* const lab = reinterpret_cast<const uint8_t*>(B.spal);
+    // write-back needed unless nothing reads these words again (even rows of the even plane, fast raster)
+    const bool keep = !(DZ == 0 && PH == 1) || !fast;
+#pragma unroll kRUnroll
+    for (uint32_t w0 = 0; w0 < HW; w0 += 32) {
+        const bool okw = HW >= 32 || lane < (int)HW;
+        const uint32_t x = okw ? *wp : 0u;
+        const uint32_t f = ((x & 0x7F7F7F7Fu) + 0x03030303u) & x & 0x80808080u;   // marker bytes (>= 253)
+        const uint32_t a0 = x << 7, a1 = x << 6;                                 // axis bits at bit 7
+        uint32_t y = x;
+        if (!K2W_RBRANCH || f) {
+            if (DZ == 0) {   // z: the previous voxel plane (final)
+                const uint32_t M = ((f & a0 & a1) >> 7) * 0xFFu;
+                if (!K2W_RBRANCH || M) y = (y & ~M) | ((okw ? *pw : 0u) & M);
+            }
+            if (PH == 1) {   // y: the odd row above (resolved in phase 0)
+                const uint32_t M = ((f & ~a0 & a1) >> 7) * 0xFFu;
+                if (!K2W_RBRANCH || M) y = (y & ~M) | ((okw ? *(wp - WPR) : 0u) & M);
+            }
+        }
+        const uint32_t left = __shfl_up_sync(FULL, y, 1);                         // x: the byte to the left
+        const uint32_t Mx = ((f & a0 & ~a1) >> 7) * 0xFFu;
+        y = (y & ~Mx) | (__byte_perm(y, left, 0x2107) & Mx);
+        if (keep && f) *wp = y;
+        if (fast && okw) {
+            const uint4 v = make_uint4(*reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y, 0, 0x4440)),
+                                       *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y, 0, 0x4441)),
+                                       *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y, 0, 0x4442)),
+                                       *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y, 0, 0x4443)));
+            __stcs(reinterpret_cast<uint4*>(op), v);   // evict-first
+            op += 2 * RPI * B.pitch;
+        }
+        wp += 2 * RPI * WPR;
+        pw += 2 * RPI * WPR;
+    }
+    __syncwarp();
+}
+
 // ---------------------------------------------------------------- final level, u8 (marker chains)
 // The u8 pass (palettes of <= 253 labels, indices <= 252) leaves every pending
 // child as the marker byte 252 + axis (e8::eval8<true>) and resolves the chains
@@ -744,8 +805,6 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
     constexpr uint32_t PP = RR * RR;           // parents per plane
     constexpr uint32_t S2 = 2 * RR;            // children (bytes) per row
     constexpr uint32_t PL = S2 * S2;           // bytes per voxel plane
-    constexpr uint32_t WPR = S2 / 4;           // words per row
-    constexpr uint32_t HW = PP / 2;            // words in the rows of one parity
     constexpr uint32_t LG = RR == 4 ? 2 : (RR == 8 ? 3 : 4);
     constexpr uint32_t MX = 0x49249u & ((1u << (3 * LG)) - 1u), MY = MX << 1, MZ = MX << 2;
     const bool leaf = B.t == 0;
@@ -844,50 +903,10 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
         }
         __syncwarp();
         // ---- marker chains, row parity by row parity; fast raster: resolve + write whole rows
-#pragma unroll 1
-        for (int dz = 0; dz < 2; ++dz) {
-            uint8_t* const pl = dz ? r1 : r0;
-            uint32_t* const zb = fast ? B.R.base + (2 * pz + dz) * B.plane : nullptr;
-#pragma unroll 1
-            for (int ph = 0; ph < 2; ++ph) {
-#pragma unroll
-                for (uint32_t w0 = 0; w0 < HW; w0 += 32) {
-                    const uint32_t wi = w0 + lane;
-                    const bool okw = wi < HW;
-                    const uint32_t row = 2 * (wi / WPR) + (ph ? 0u : 1u), cw = wi % WPR;
-                    uint32_t* const wp = reinterpret_cast<uint32_t*>(pl + row * S2) + cw;
-                    const uint32_t x = okw ? *wp : 0u;
-                    const uint32_t f = ((x & 0x7F7F7F7Fu) + 0x03030303u) & x & 0x80808080u;   // bytes >= 253
-                    const uint32_t a0 = x << 7, a1 = x << 6;                                 // axis bits at bit 7
-                    uint32_t y = x;
-                    if (f) {
-                        const uint32_t mz = dz == 0 ? f & a0 & a1 : 0u;
-                        if (mz) {
-                            const uint32_t M = (mz >> 7) * 0xFFu;
-                            y = (y & ~M) | (*reinterpret_cast<const uint32_t*>(pr + row * S2 + 4 * cw) & M);
-                        }
-                        const uint32_t my = ph ? f & ~a0 & a1 : 0u;
-                        if (my) {
-                            const uint32_t M = (my >> 7) * 0xFFu;
-                            y = (y & ~M) | (*(wp - WPR) & M);
-                        }
-                    }
-                    const uint32_t left = __shfl_up_sync(FULL, y, 1);
-                    const uint32_t mx = f & a0 & ~a1;
-                    if (mx) {
-                        const uint32_t M = (mx >> 7) * 0xFFu;
-                        y = (y & ~M) | (__byte_perm(y, left, 0x2107) & M);
-                    }
-                    if (f) *wp = y;
-                    if (fast && okw) {
-                        const uint4 lab = make_uint4(label_of<uint8_t>(B, y & 0xFFu), label_of<uint8_t>(B, (y >> 8) & 0xFFu), label_of<uint8_t>(B, (y >> 16) & 0xFFu),
-                                                     label_of<uint8_t>(B, y >> 24));
-                        __stcs(reinterpret_cast<uint4*>(zb + row * B.pitch + 4 * cw), lab);   // evict-first
-                    }
-                }
-                __syncwarp();
-            }
-        }
+        resolve_rows<RR, 0, 0>(B, r0, pr, fast, fast ? B.R.base + (2 * pz) * B.plane : nullptr, lane);
+        resolve_rows<RR, 0, 1>(B, r0, pr, fast, fast ? B.R.base + (2 * pz) * B.plane : nullptr, lane);
+        resolve_rows<RR, 1, 0>(B, r1, pr, fast, fast ? B.R.base + (2 * pz + 1) * B.plane : nullptr, lane);
+        resolve_rows<RR, 1, 1>(B, r1, pr, fast, fast ? B.R.base + (2 * pz + 1) * B.plane : nullptr, lane);
         if (!fast) {
             if (MODE == OUT_RASTER) {
 #pragma unroll 1
