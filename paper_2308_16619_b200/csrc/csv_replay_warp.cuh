@@ -495,6 +495,9 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
     return warp_min64(ek);
 }
 
+__host__ __device__ __forceinline__ constexpr uint32_t spread3_c(uint32_t v) {   // spread3 of a (compile-time) coordinate < 32
+    return (v & 1u) | ((v & 2u) << 2) | ((v & 4u) << 4) | ((v & 8u) << 6) | ((v & 16u) << 8);
+}
 // ---------------------------------------------------------------- final level (plane sweep)
 // offset of child c (x, y bits) of plane parent i = px + RR * py inside a ring voxel plane
 template <int RR>
@@ -833,6 +836,7 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
     }
     __syncwarp();
     const bool fast = MODE == OUT_RASTER && B.al16r;
+    const uint32_t qlane = spread3_u32(lane % RR) | (spread3_u32((lane / RR) % RR) << 1);
 #pragma unroll 1
     for (uint32_t pz = 0; pz < RR; ++pz) {
         const uint32_t sz = spread3_u32(pz) << 2;
@@ -848,7 +852,9 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
             const uint32_t i = i0 + lane;
             const bool ok = i < PP;
             const uint32_t px = i % RR, py = i / RR;
-            const uint32_t q = spread3_u32(px) | (spread3_u32(py) << 1) | sz;
+            // i0 / RR and lane / RR have disjoint bits: the Morton code splits into a
+            // per-lane part and a compile-time part of this (unrolled) iteration
+            const uint32_t q = qlane | (spread3_c(i0 / RR) << 1) | sz;
             uint32_t mw = 0, pv = 0;
             if (ok) {
                 pv = plev[q];
@@ -890,7 +896,7 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
                 const uint32_t pxp = plev[morton_inc(q, MX)];
                 const uint32_t pyp = plev[morton_inc(q, MY)];
                 const uint32_t pzp = plev[morton_inc(q, MZ)];
-                const int32_t ipq = (w & 0x0404040404040404ull) ? (int32_t)B.ipb[rank] : 0;   // palette ops only
+                const int32_t ipq = B.ipb[rank];   // (issued with the entry load, not after it)
                 e8::Out g;
                 e8::eval8<true>(w, pv, pxp, pyp, pzp, bf, ipq, B.plen, vmask, leaf, g);
                 pdl += g.n5;
