@@ -155,6 +155,15 @@ int csv_decode_volume_range(csv_volume* vol, int t, uint64_t brick_first, uint64
 int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, const uint8_t* d_lod,
                       const uint64_t* d_dst, uint32_t* d_pool, csv_result* d_res, uintptr_t stream);
 
+/* Host-buffer variant of csv_decode_bricks for per-brick callers
+ * (CsvContainer.decode_brick, container.py:168-208, on a device-resident volume):
+ * n (brick, lod) requests in host memory; the Morton labels land in h_out
+ * contiguously in request order (8^(N - lod) each), per-request results in
+ * h_res.  Requests are staged through library-owned pinned memory; the call
+ * returns after the stream has synchronised. */
+int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick, const uint8_t* h_lod,
+                           uint32_t* h_out, csv_result* h_res, uintptr_t stream);
+
 /* Stand-alone entropy stage (K1): replaces rans_decode/_decode_core
  * (rans.py:140-198) + iter_operations (codec.py:604-623).  For each request
  * brick, decodes the coarse and (t == 0) detail stream into entry bytes
@@ -213,6 +222,38 @@ int csv_encoded_free(csv_encoded* enc);
  * seeds per drift_seed (time series).  d_out: (Z,Y,X) u32. */
 int csv_synth_voronoi(uint32_t* d_out, int64_t X, int64_t Y, int64_t Z, int cells_per_axis, uint32_t seed,
                       int membrane, double drift, uint32_t drift_seed, uintptr_t stream);
+
+/* ---------------------------------------------------------------- raw rANS coder and pyramid
+ * The stand-alone pieces of the reference's public API that are not the fused
+ * decode (csv_rans.cu). */
+
+/* rans_decode (rans.py:183-198, _decode_core :140-165): stream i is
+ * d_nbytes[i] bytes at d_data + d_off[i]; exactly d_nsym[i] raw nibbles go to
+ * d_out + d_out_off[i].  counts16: the 16 quantized counts (sum 4096).
+ * d_status[2i] = 0 ok / 1 truncated / 2 desynchronized, d_status[2i+1] = the
+ * symbol position of the reference's message ("truncated at symbol {pos}",
+ * "desynchronized after {n} symbols"). */
+int csv_rans_decode(const uint8_t* d_data, const uint64_t* d_off, const uint32_t* d_nbytes, const uint32_t* d_nsym,
+                    uint64_t n_streams, const uint16_t* counts16, uint8_t* d_out, const uint64_t* d_out_off,
+                    int32_t* d_status, uintptr_t stream);
+/* rans_encode (rans.py:168-180, _encode_core :120-137): stream i's d_nsym[i]
+ * nibbles (< 16) at d_nibbles + d_off[i] are coded into the back of a
+ * 2 * nsym + 8 byte slot at d_buf + d_buf_off[i]; the stream is
+ * [d_start[i], 2 * nsym + 8) of the slot, byte-identical to the reference.
+ * Every coded symbol must have a nonzero count (the caller checks, as
+ * rans_encode does). */
+int csv_rans_encode(const uint8_t* d_nibbles, const uint64_t* d_off, const uint32_t* d_nsym, uint64_t n_streams,
+                    const uint16_t* counts16, uint8_t* d_buf, const uint64_t* d_buf_off, uint32_t* d_start,
+                    uintptr_t stream);
+/* build_pyramid (pyramid.py:65-78): n_bricks Morton-ordered bricks of 8^N labels
+ * (d_labels, contiguous) -> per brick the levels 0..N concatenated
+ * (sum 8^l entries, level 0 first) in d_levels and the subtree-constant flags
+ * (u8) in d_const, same layout. */
+int csv_build_pyramid(const uint32_t* d_labels, uint64_t n_bricks, int brick_log2, uint32_t* d_levels,
+                      uint8_t* d_const, uintptr_t stream);
+/* downsample_level (pyramid.py:81-96): (nz, ny, nx) u32 grid, even sides ->
+ * (nz/2, ny/2, nx/2), mode of each 2x2x2 cell with first-occurrence ties. */
+int csv_downsample(const uint32_t* d_in, int64_t nz, int64_t ny, int64_t nx, uint32_t* d_out, uintptr_t stream);
 
 /* ---------------------------------------------------------------- frame bookkeeping
  * Device restatements of the steps around the batched cache decode. */

@@ -7,7 +7,7 @@ kernels (csrc/) reached through the C-ABI in include/csvgpu.h.
 """
 
 from .cache import BrickCache, CacheStats, DeviceBrickCache
-from .codec import BrickEncoding, decode_brick, decode_brick_entropy, decode_root, iter_operations
+from .codec import BrickEncoding, decode_brick, decode_brick_entropy, decode_root, encode_brick, iter_operations
 from .container import (CompressionConfig, CsvContainer, VolumeMeta, decompress_volume,
                         decompress_volume_device, stats)
 from .detail import DetailStore, DeviceDetailStream
@@ -17,7 +17,8 @@ from .encode import GpuEncoded, compress_volume, compress_volume_device, synth_v
 from .errors import (CacheCapacityError, ConfigError, CorruptStreamError, CsvolError, EncodabilityError,
                      IngestionError)
 from .morton import BrickConfig, NodeCoord, morton_decode, morton_encode, outside_neighbor
-from .rans import FrequencyTable, TablePair, build_frequency_tables, quantize_counts
+from .pyramid import Pyramid, build_pyramid, downsample_level, downsample_volume, pyramid_from_grid
+from .rans import FrequencyTable, TablePair, build_frequency_tables, quantize_counts, rans_decode, rans_encode
 
 __version__ = "0.1.0"
 
@@ -28,4 +29,6 @@ __all__ = [
     "GpuEncoded", "GpuVolume", "compress_volume", "compress_volume_device", "synth_voronoi", "IngestionError", "NodeCoord", "TablePair", "VolumeMeta", "build_frequency_tables",
     "decode_brick", "decode_brick_entropy", "decode_root", "decompress_volume", "decompress_volume_device",
     "iter_operations", "stats", "morton_decode", "morton_encode", "outside_neighbor", "quantize_counts",
+    "encode_brick", "Pyramid", "build_pyramid", "downsample_level", "downsample_volume", "pyramid_from_grid",
+    "rans_decode", "rans_encode",
 ]

@@ -31,7 +31,8 @@ EXPORTS = (
     "csv_desired_lods", "csv_visibility_mask", "csv_cache_create", "csv_cache_free", "csv_cache_begin_frame",
     "csv_cache_mark_used", "csv_cache_assign", "csv_cache_state", "csv_cache_counters", "csv_cache_stack_heights",
     "csv_cache_read_state", "csv_cache_plan", "csv_cache_decode_fills", "csv_volume_stage_detail",
-    "csv_cache_read_fills", "csv_detail_plan_greedy",
+    "csv_cache_read_fills", "csv_detail_plan_greedy", "csv_rans_decode", "csv_rans_encode", "csv_build_pyramid",
+    "csv_downsample", "csv_decode_bricks_host",
 )
 
 
@@ -129,6 +130,16 @@ def lib():
         L.csv_cache_counters.argtypes = [P, P]
         L.csv_cache_stack_heights.restype = I
         L.csv_cache_stack_heights.argtypes = [P, P]
+        L.csv_rans_decode.restype = I
+        L.csv_rans_decode.argtypes = [P, P, P, P, U64, P, P, P, P, UP]
+        L.csv_rans_encode.restype = I
+        L.csv_rans_encode.argtypes = [P, P, P, U64, P, P, P, P, UP]
+        L.csv_build_pyramid.restype = I
+        L.csv_build_pyramid.argtypes = [P, U64, I, P, P, UP]
+        L.csv_decode_bricks_host.restype = I
+        L.csv_decode_bricks_host.argtypes = [P, U64, P, P, P, P, UP]
+        L.csv_downsample.restype = I
+        L.csv_downsample.argtypes = [P, I64, I64, I64, P, UP]
         _lib = L
     return _lib
 

@@ -156,6 +156,37 @@ def decode_brick_entropy(palette, coarse_bytes, coarse_nibbles: int, detail_byte
                        config, t, return_consumed)
 
 
+def encode_brick(pyramid, config: BrickConfig | None = None) -> BrickEncoding:
+    """Encode a pyramid into palette + coarse/detail nibble streams (codec.py:224-235).
+
+    Runs the GPU encoder's per-brick stages (csv_encode_volume: E1 pyramid, E2
+    greedy operations + palette replay, raw nibble packing) on the brick's
+    level-0 labels.  Those stages re-derive levels 1..N, so ``pyramid`` must
+    be the reference rule's pyramid of its level 0 (what build_pyramid
+    returns); any other pyramid is refused with ValueError rather than encoded
+    differently from the reference.
+    """
+    from .container import CompressionConfig
+    from .encode import compress_volume
+    from .morton import morton_to_grid
+    from .pyramid import build_pyramid
+    config = config or pyramid.config
+    n = config.brick_log2
+    level0 = np.ascontiguousarray(pyramid.levels[0], dtype=np.uint32)
+    if level0.shape != (8 ** n,) or len(pyramid.levels) != n + 1:
+        raise ValueError(f"pyramid does not match b={config.side}")
+    ref = build_pyramid(level0, config)
+    if any(not np.array_equal(np.asarray(a), b) for a, b in zip(pyramid.levels, ref.levels)) or \
+            any(not np.array_equal(np.asarray(a, dtype=bool), b) for a, b in zip(pyramid.constant, ref.constant)):
+        raise ValueError("pyramid is not the mode-of-8 pyramid of its level 0 (build_pyramid)")
+    grid = morton_to_grid(level0, config.side)
+    c = compress_volume(grid, CompressionConfig(brick_log2=n, entropy=False))
+    e = c.directory[0]
+    coarse = unpack_nibbles(c.brick_coarse(0), int(e["coarse_nibbles"]))
+    detail = unpack_nibbles(c.brick_detail(0), int(e["detail_nibbles"]))
+    return BrickEncoding(n, c.brick_palette(0).astype(np.uint32).copy(), coarse.copy(), detail.copy())
+
+
 def decode_root(encoding: BrickEncoding) -> int:
     """Coarsest-LOD label (codec.py:597-601)."""
     if encoding.palette.size == 0:

@@ -99,7 +99,7 @@ class CsvContainer:
     detail_blob: np.ndarray | None
     _detail_file: Path | None = field(default=None, repr=False)
     _detail_base: int = field(default=0, repr=False)
-    _gpu: object = field(default=None, repr=False)
+    _gpu: object = field(default=None, repr=False, init=False, compare=False)   # (key, GpuVolume) of _device_volume
 
     @property
     def config(self) -> BrickConfig:
@@ -159,6 +159,8 @@ class CsvContainer:
             if t > cfg.brick_log2:
                 raise ValueError(f"LOD {t} above coarsest level {cfg.brick_log2}")
             return lab
+        if detail is None and (t > 0 or self.detail_blob is not None):
+            return self._decode_resident(index, t)
         if t == 0:
             if detail is None:
                 detail = self.brick_detail(index)
@@ -173,6 +175,35 @@ class CsvContainer:
         enc = BrickEncoding(cfg.brick_log2, self.brick_palette(index),
                             unpack_nibbles(coarse, int(e["coarse_nibbles"])), unpack_nibbles(detail, n_detail))
         return codec.decode_brick(enc, t, cfg)
+
+    def _device_volume(self):
+        """The container resident in HBM (uploaded on first use, reused by every
+        decode_brick call; re-uploaded if the directory or a blob is replaced)."""
+        key = (id(self.directory), id(self.palette_blob), id(self.coarse_blob), id(self.detail_blob))
+        if self._gpu is None or self._gpu[0] != key:
+            if self._gpu is not None:
+                self._gpu[1].close()
+            self._gpu = (key, self.to_device())
+        return self._gpu[1]
+
+    def _decode_resident(self, index: int, t: int) -> np.ndarray:
+        """One brick from the device-resident container: one C-ABI call
+        (csv_decode_bricks_host: pinned request copy, K1 + K2w, label copy-back)."""
+        from . import _lib
+        from .device import status_error
+        vol = self._device_volume()
+        torch = vol._torch
+        out = np.empty(8 ** (self.meta.brick_log2 - t), dtype=np.uint32)
+        res = np.zeros(1, dtype=_lib.RESULT_DTYPE)
+        req_b = np.array([index], dtype=np.uint32)
+        req_l = np.array([t], dtype=np.uint8)
+        with torch.cuda.device(vol.device):
+            _lib.check(_lib.lib().csv_decode_bricks_host(vol._h, 1, req_b.ctypes.data, req_l.ctypes.data,
+                                                          out.ctypes.data, res.ctypes.data,
+                                                          torch.cuda.current_stream(vol.device).cuda_stream))
+        if res["status"][0] != 0:
+            raise status_error(int(res["status"][0]), int(res["stream"][0]), int(res["pos"][0]))
+        return out
 
     # -- sizes -----------------------------------------------------------------
     @property

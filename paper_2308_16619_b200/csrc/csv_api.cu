@@ -73,6 +73,12 @@ struct csv_volume {
     uint64_t blob_cap[3]{};         // bytes of the palette / coarse / detail slices held
     bool timing = false;
     cudaEvent_t ev[4]{};            // plan start, K1 start, K1 end / K2 start, K2 end
+    // csv_decode_bricks_host: pinned request staging + device requests / pool / results (grow-only)
+    uint64_t hreq_cap = 0, hpool_cap = 0;
+    uint8_t* h_req = nullptr;       // pinned: brick u32[cap] | lod u8[cap] (16-aligned) | dst u64[cap]
+    uint8_t* d_req = nullptr;       // same layout on the device
+    csv_result* d_hres = nullptr;
+    uint32_t* d_hpool = nullptr;
 };
 
 // ---------------------------------------------------------------------------- kernels local to the API
@@ -213,6 +219,8 @@ static void vol_release(csv_volume* v) {
     dfree(v->d_soa); dfree(v->d_blob); dfree(v->d_dtab);
     dfree(v->d_sizes); dfree(v->d_eoff); dfree(v->d_scan); dfree(v->d_sres);
     dfree(v->d_counter); dfree(v->d_entries); dfree(v->d_gws); dfree(v->d_wscratch);
+    dfree(v->d_req); dfree(v->d_hres); dfree(v->d_hpool);
+    if (v->h_req) cudaFreeHost(v->h_req);
     cudaStreamSynchronize(0);
     for (auto& e : v->ev) if (e) cudaEventDestroy(e);
     delete v;
@@ -536,6 +544,58 @@ int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, cons
     P.wscratch_stride = kWScratchStride;
     CUDA_TRY(run_decode(vol->V, P, 1, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
                         vol->gws_ctas, vol->nsm, 0, st, vol->timing ? vol->ev : nullptr));
+    return CSV_OK;
+}
+
+// Per-brick host API: requests and labels in host memory, one call per batch
+// (CsvContainer.decode_brick's device-resident path).  Requests go through a
+// pinned staging buffer in one copy; outputs land contiguously in request order.
+int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick, const uint8_t* h_lod,
+                           uint32_t* h_out, csv_result* h_res, uintptr_t stream) {
+    if (!vol || (n && (!h_brick || !h_lod || !h_out || !h_res))) return fail(CSV_E_ARG, "null argument");
+    if (n == 0) return CSV_OK;
+    CUDA_TRY(cudaSetDevice(vol->device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const uint64_t lod_off = (4 * n + 15) & ~15ull, dst_off = (lod_off + n + 15) & ~15ull, req_bytes = dst_off + 8 * n;
+    if (n > vol->hreq_cap) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (vol->h_req) cudaFreeHost(vol->h_req);
+        vol->h_req = nullptr;
+        dfree(vol->d_req); dfree(vol->d_hres);
+        vol->hreq_cap = 0;
+        const uint64_t cap = std::max<uint64_t>(n, 64);
+        const uint64_t bytes = ((4 * cap + 15) & ~15ull) + ((cap + 15) & ~15ull) + 8 * cap + 32;
+        CUDA_TRY(cudaMallocHost(&vol->h_req, bytes));
+        CUDA_TRY(dalloc(&vol->d_req, bytes, st));
+        CUDA_TRY(dalloc(&vol->d_hres, cap * sizeof(csv_result), st));
+        vol->hreq_cap = cap;
+    }
+    uint8_t* h = vol->h_req;
+    uint64_t* dst = reinterpret_cast<uint64_t*>(h + dst_off);
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const int t = h_lod[i];
+        if (t > vol->V.N) return fail(CSV_E_ARG, "LOD %d outside [0, %d]", t, vol->V.N);
+        dst[i] = total;
+        total += 1ull << (3 * (vol->V.N - t));
+    }
+    if (total > vol->hpool_cap) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        dfree(vol->d_hpool);
+        vol->hpool_cap = 0;
+        CUDA_TRY(dalloc(&vol->d_hpool, total * sizeof(uint32_t), st));
+        vol->hpool_cap = total;
+    }
+    memcpy(h, h_brick, 4 * n);
+    memcpy(h + lod_off, h_lod, n);
+    CUDA_TRY(cudaMemcpyAsync(vol->d_req, h, req_bytes, cudaMemcpyHostToDevice, st));
+    const int rc = csv_decode_bricks(vol, n, reinterpret_cast<const uint32_t*>(vol->d_req), vol->d_req + lod_off,
+                                     reinterpret_cast<const uint64_t*>(vol->d_req + dst_off), vol->d_hpool, vol->d_hres,
+                                     stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(h_res, vol->d_hres, n * sizeof(csv_result), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h_out, vol->d_hpool, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     return CSV_OK;
 }
 

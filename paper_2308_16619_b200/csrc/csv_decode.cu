@@ -73,6 +73,40 @@ __device__ uint64_t block_excl_scan(uint64_t v, uint64_t* sh, uint64_t* total) {
     return r;
 }
 
+// Small plans (2n <= SCAN_ITEMS streams): region sizes + exclusive scan + the K1/K2w
+// work counters in ONE launch (per-brick calls are launch-latency bound).
+__global__ void __launch_bounds__(256) k_plan_small(VolView V, Plan P, unsigned long long* counter) {
+    __shared__ uint64_t sh[33];
+    constexpr int PER = SCAN_ITEMS / 256;
+    const uint64_t n2 = 2 * P.n;
+    uint64_t loc[PER];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const uint64_t i = threadIdx.x * PER + k;
+        uint64_t v = 0;
+        if (i < n2) {
+            const uint64_t b = req_local(V, P, i >> 1);
+            const int t = req_lod(P, i >> 1);
+            v = round32((b < V.nb && t < V.N) ? stream_limit(V, b, t, (int)(i & 1)) : 0);
+        }
+        loc[k] = v;
+        sum += v;
+    }
+    uint64_t tot;
+    uint64_t pre = block_excl_scan(sum, sh, &tot);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const uint64_t i = threadIdx.x * PER + k;
+        if (i < n2) P.eoff[i] = pre;
+        pre += loc[k];
+    }
+    if (threadIdx.x == 0) {
+        P.eoff[n2] = tot;
+        counter[0] = counter[1] = counter[2] = 0;
+    }
+}
+
 __global__ void k_scan_blocks(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* block_sums) {
     __shared__ uint64_t sh[33];
     uint64_t base = (uint64_t)blockIdx.x * SCAN_ITEMS;
@@ -1032,11 +1066,15 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
                        int nsm, int min_t, cudaStream_t st, cudaEvent_t* ev) {
     if (P.n == 0) return cudaSuccess;
     if (ev) cudaEventRecord(ev[0], st);
-    unsigned nb = (unsigned)((2 * P.n + 255) / 256);
-    k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
-    cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
-    if (e != cudaSuccess) return e;
-    cudaMemsetAsync(counter, 0, 3 * sizeof(unsigned long long), st);   // K1 items, K2w u8 / u16 bricks
+    if (2 * P.n <= (uint64_t)SCAN_ITEMS) {
+        k_plan_small<<<1, 256, 0, st>>>(V, P, counter);
+    } else {
+        unsigned nb = (unsigned)((2 * P.n + 255) / 256);
+        k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
+        cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
+        if (e != cudaSuccess) return e;
+        cudaMemsetAsync(counter, 0, 3 * sizeof(unsigned long long), st);   // K1 items, K2w u8 / u16 bricks
+    }
     if (ev) cudaEventRecord(ev[1], st);
     if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
     else launch_k1<false>(V, P, counter, nsm, st);

@@ -55,7 +55,9 @@ class TransferFunction:
 def _volume(v):
     if isinstance(v, GpuVolume):
         return v, False
-    return v.to_device(), True          # a CsvContainer: upload once for this call
+    # a CsvContainer: upload directory + palettes for this call (geometry and
+    # palettes are all these kernels read; the detail section stays on the host)
+    return v.to_device(cold_detail=True), True
 
 
 def desired_lods_device(volume: GpuVolume, camera: Camera, out=None, stream=None):

@@ -103,3 +103,75 @@ def packed_decode_table(table: FrequencyTable) -> np.ndarray:
         slots = np.arange(f, dtype=np.uint32)
         out[cum[s]: cum[s] + f] = (np.uint32(f) << np.uint32(16)) | (slots << np.uint32(4)) | np.uint32(s)
     return out
+
+
+# ------------------------------------------------------------------ raw-nibble coder (GPU)
+def _streams_on_device(torch, arrays):
+    """Concatenate byte arrays into one device buffer: (buffer, offsets u64, sizes u32)."""
+    sizes = np.array([a.size for a in arrays], dtype=np.uint32)
+    offs = np.zeros(len(arrays), dtype=np.uint64)
+    if len(arrays) > 1:
+        offs[1:] = np.cumsum(sizes[:-1], dtype=np.uint64)
+    flat = np.concatenate([np.asarray(a, dtype=np.uint8) for a in arrays] + [np.zeros(16, np.uint8)])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return (torch.from_numpy(flat).to(dev), torch.from_numpy(offs.view(np.int64)).to(dev),
+            torch.from_numpy(sizes.view(np.int32)).to(dev), dev)
+
+
+def rans_decode(data: bytes, n_symbols: int, table: FrequencyTable) -> np.ndarray:
+    """Decode exactly ``n_symbols`` nibbles and verify stream integrity (rans.py:183-198).
+
+    Runs on the GPU (csv_rans_decode, one lane per stream); the reference's
+    CorruptStreamError messages for truncated and desynchronized streams.
+    """
+    from . import _lib
+    from .errors import CorruptStreamError
+    torch = _lib.require_cuda()
+    n_symbols = int(n_symbols)
+    if n_symbols < 0:
+        raise ValueError("negative symbol count")
+    raw = np.frombuffer(bytes(data), dtype=np.uint8)
+    buf, off, nb, dev = _streams_on_device(torch, [raw])
+    nsym = torch.tensor([n_symbols], dtype=torch.int32, device=dev)
+    out = torch.empty(max(n_symbols, 1), dtype=torch.uint8, device=dev)
+    out_off = torch.zeros(1, dtype=torch.int64, device=dev)
+    status = torch.empty(2, dtype=torch.int32, device=dev)
+    counts = np.ascontiguousarray(table.counts, dtype=np.uint16)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().csv_rans_decode(buf.data_ptr(), off.data_ptr(), nb.data_ptr(), nsym.data_ptr(), 1,
+                                              counts.ctypes.data, out.data_ptr(), out_off.data_ptr(),
+                                              status.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    st, pos = (int(v) for v in status.cpu().tolist())
+    if st == 1:
+        raise CorruptStreamError(f"entropy stream truncated at symbol {pos}")
+    if st == 2:
+        raise CorruptStreamError(f"entropy stream desynchronized after {n_symbols} symbols")
+    return out[:n_symbols].cpu().numpy()
+
+
+def rans_encode(nibbles, table: FrequencyTable) -> bytes:
+    """Entropy-code a nibble sequence; deterministic and byte-exact (rans.py:168-180).
+
+    The encodability check is the reference's (host); the coding runs on the
+    GPU (csv_rans_encode)."""
+    from . import _lib
+    from .errors import EncodabilityError
+    torch = _lib.require_cuda()
+    arr = np.ascontiguousarray(nibbles, dtype=np.uint8)
+    counts = np.ascontiguousarray(table.counts, dtype=np.uint16)
+    if arr.size and (arr.max() >= NUM_SYMBOLS or counts[np.minimum(arr, 15)].min() == 0):
+        bad = int(np.flatnonzero((arr >= NUM_SYMBOLS) | (counts[np.minimum(arr, 15)] == 0))[0])
+        raise EncodabilityError(f"nibble {int(arr[bad])} at position {bad} has zero frequency")
+    buf, off, _, dev = _streams_on_device(torch, [arr])
+    nsym = torch.tensor([arr.size], dtype=torch.int32, device=dev)
+    cap = 2 * arr.size + 8
+    out = torch.empty(cap, dtype=torch.uint8, device=dev)
+    out_off = torch.zeros(1, dtype=torch.int64, device=dev)
+    start = torch.empty(1, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().csv_rans_encode(buf.data_ptr(), off.data_ptr(), nsym.data_ptr(), 1, counts.ctypes.data,
+                                              out.data_ptr(), out_off.data_ptr(), start.data_ptr(),
+                                              torch.cuda.current_stream(dev).cuda_stream))
+    s0 = int(start.item())
+    return out[s0:cap].cpu().numpy().tobytes()
+

@@ -121,6 +121,36 @@ def test_fuzz_error_parity(pkg, name):
             assert got == exp, (name, case, t)
 
 
+@pytest.mark.parametrize("name", ["d_b5_mem", "e_b4_raw"])
+def test_fuzz_resident_decode_brick(pkg, name):
+    """CsvContainer.decode_brick on the device-resident container (csv_decode_bricks_host)
+    raises the reference's exact message, or returns its labels, for corrupted streams."""
+    base = golden_bytes(name)
+    for case in golden_json(f"fuzz_{name}.json")[:80]:
+        c = pkg.CsvContainer.from_bytes(fuzz_container_bytes(base, case))
+        if case["dir"]:
+            d = c.directory.copy()
+            d[case["brick"]][case["dir"][0]] = case["dir"][1]
+            c.directory = d
+        for t, exp in case["outcomes"].items():
+            assert _gpu_outcome(pkg, c, case["brick"], int(t)) == exp[:2], (name, case, t)
+
+
+def test_resident_container_follows_replacement(pkg):
+    """The cached device copy is rebuilt when the directory or a blob is replaced."""
+    g = golden_json("decode_d_b5_mem.json")
+    c = pkg.CsvContainer.from_bytes(golden_bytes("d_b5_mem"))
+    i = int(list(g["bricks"])[1])
+    assert h16(c.decode_brick(i, 0)) == g["bricks"][str(i)]["0"][1]
+    d = c.directory.copy()
+    d[i]["detail_bytes"] = 2          # truncated detail stream: decode must now fail
+    c.directory = d
+    with pytest.raises(pkg.CorruptStreamError):
+        c.decode_brick(i, 0)
+    c2 = pkg.CsvContainer.from_bytes(golden_bytes("d_b5_mem"))
+    assert h16(c2.decode_brick(i, 1)) == g["bricks"][str(i)]["1"][1]
+
+
 def test_config1_full_volume(pkg):
     cfg = golden_json("config1.json")
     with open(GOLDEN + "/config1.csv1", "rb") as f:

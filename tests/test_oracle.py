@@ -110,3 +110,40 @@ def test_config1_generator_and_encoder(oracle):
     assert hashlib.sha256(vol.astype("<u4").tobytes()).hexdigest()[:16] == cfg["input_sha"] == "70906f1c5d15fbda"
     c = oracle.compress_volume(vol, brick_log2=5)
     assert hashlib.sha256(c.to_bytes()).hexdigest()[:16] == cfg["container_sha"]
+
+
+def test_oracle_dropin_goldens(oracle):
+    """The oracle's rANS coder, pyramid and per-brick encoder against the reference's
+    own outputs for the stand-alone drop-ins (tests/golden/dropin.json)."""
+    import os
+    from conftest import GOLDEN, golden_json, h16
+    G = golden_json("dropin.json")
+    for case in G["rans"]:
+        counts = np.array(case["counts"], dtype=np.uint16)
+        nib = np.frombuffer(bytes.fromhex(case["nibbles"]), dtype=np.uint8)
+        data = bytes.fromhex(case["encoded"])
+        assert oracle.rans_encode(nib, counts) == data
+        st, where, out = oracle.rans_decode(data, nib.size, counts)
+        assert st == 0 and h16(out) == case["decode"]["exact"]["ok"]
+        st, where, _ = oracle.rans_decode(data[:-1], nib.size, counts)
+        exp = case["decode"]["short"]
+        if "error" in exp:
+            assert st == 1 and exp["error"] == f"entropy stream truncated at symbol {where}"
+    for case, enc in zip(G["pyramid"], G["encode"]):
+        N = case["brick_log2"]
+        src = case["source"]
+        if "labels" in src:
+            flat = np.frombuffer(bytes.fromhex(src["labels"]), dtype="<u4").astype(np.uint32)
+        else:
+            vol = np.load(os.path.join(GOLDEN, f"vol_{src['vol']}.npz"))["volume"]
+            b = 1 << N
+            z, y, x = src["zyx"]
+            grid = np.zeros((b, b, b), dtype=np.uint32)
+            piece = vol[z:z + b, y:y + b, x:x + b]
+            grid[:piece.shape[0], :piece.shape[1], :piece.shape[2]] = piece
+            flat = np.empty(b ** 3, dtype=np.uint32)
+            flat[oracle.morton_codes(b)] = grid.ravel()
+        assert [h16(oracle.pyramid_level(flat, N, t)) for t in range(N + 1)] == case["levels"], case["name"]
+        pal, co, de = oracle.encode_brick(flat, N)
+        assert (h16(pal), pal.size, h16(co), co.size, h16(de), de.size) == \
+            (enc["palette"], enc["n_palette"], enc["coarse"], enc["n_coarse"], enc["detail"], enc["n_detail"])
