@@ -63,6 +63,7 @@ struct csv_volume {
     uint64_t entries_cap = 0;
     uint32_t* d_gws = nullptr;
     uint16_t* d_wscratch = nullptr;  // K2w per-warp palette bases (nsm x 64 warps x 4096)
+    uint16_t* d_wscratch6 = nullptr; // K2w<6> per-warp slots (nsm x 8 warps x kWScratch6Stride), N >= 6 only
     uint64_t gws_stride = 0;
     int gws_ctas = 0;
     uint64_t gws_words_cap = 0;
@@ -218,7 +219,7 @@ static void vol_release(csv_volume* v) {
     cudaDeviceSynchronize();
     dfree(v->d_soa); dfree(v->d_blob); dfree(v->d_dtab);
     dfree(v->d_sizes); dfree(v->d_eoff); dfree(v->d_scan); dfree(v->d_sres);
-    dfree(v->d_counter); dfree(v->d_entries); dfree(v->d_gws); dfree(v->d_wscratch);
+    dfree(v->d_counter); dfree(v->d_entries); dfree(v->d_gws); dfree(v->d_wscratch); dfree(v->d_wscratch6);
     dfree(v->d_req); dfree(v->d_hres); dfree(v->d_hpool);
     if (v->h_req) cudaFreeHost(v->h_req);
     cudaStreamSynchronize(0);
@@ -238,6 +239,8 @@ static int ensure_plan(csv_volume* v, uint64_t n, uint64_t entries_need, int Lg,
         v->plan_cap = cap;
     }
     if (!v->d_wscratch) CUDA_TRY(dalloc(&v->d_wscratch, (size_t)v->nsm * 64 * kWScratchStride * sizeof(uint16_t), st));
+    if (!v->d_wscratch6 && v->V.N >= 6)
+        CUDA_TRY(dalloc(&v->d_wscratch6, (size_t)v->nsm * kK2W6MaxWarpsPerSM * kWScratch6Stride * sizeof(uint16_t), st));
     if (!v->d_scan) {
         CUDA_TRY(dalloc(&v->d_scan, 4104 * sizeof(uint64_t), st));
         CUDA_TRY(dalloc(&v->d_counter, 4 * sizeof(unsigned long long), st));
@@ -509,6 +512,7 @@ int csv_decode_volume_range(csv_volume* vol, int t, uint64_t brick_first, uint64
     P.entries = vol->d_entries;
     P.wscratch = vol->d_wscratch;
     P.wscratch_stride = kWScratchStride;
+    P.wscratch6 = vol->d_wscratch6;
     CUDA_TRY(run_decode(vol->V, P, 0, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
                         vol->gws_ctas, vol->nsm, t, st, vol->timing ? vol->ev : nullptr));
     return CSV_OK;
@@ -542,6 +546,7 @@ int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, cons
     P.entries = vol->d_entries;
     P.wscratch = vol->d_wscratch;
     P.wscratch_stride = kWScratchStride;
+    P.wscratch6 = vol->d_wscratch6;
     CUDA_TRY(run_decode(vol->V, P, 1, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
                         vol->gws_ctas, vol->nsm, 0, st, vol->timing ? vol->ev : nullptr));
     return CSV_OK;

@@ -25,6 +25,7 @@
 #include <cstring>
 #include <type_traits>
 #include "csv_device.cuh"
+#include "csv_eval8.cuh"
 
 namespace csv {
 
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(256) k_plan_small(VolView V, Plan P, unsigned 
     }
     if (threadIdx.x == 0) {
         P.eoff[n2] = tot;
-        counter[0] = counter[1] = counter[2] = 0;
+        counter[0] = counter[1] = counter[2] = counter[3] = 0;
     }
 }
 
@@ -657,6 +658,7 @@ k2_replay(VolView V, Plan P, uint32_t* gws, uint64_t ws_stride) {
             R.fast = R.ox + side <= P.cx && R.oy + side <= P.cy && R.oz >= P.z_begin && R.oz + side <= P.z_end &&
                      (uint64_t)P.cx * P.cy * side < (1ull << 32);
         }
+        if (LMAX == 6 && P.k2w6 && plen <= e8::kMarkPal) continue;   // decoded by K2w<6>
         if (plen == 0) { write_result(P, r, CSV_ST_EMPTY_PALETTE, 0, 0, 0, 0); continue; }
         if (t == N) {   // coarsest LOD: palette[0] (codec.py:514-516, container.py:178-182)
             if (threadIdx.x == 0) {
@@ -1034,6 +1036,7 @@ static void k2w_launch_one(const VolView& V, const Plan& P, unsigned long long* 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_warp<MODE, L, IT>, 32 * K2W_WARPS, smem);
         if (occ < 1) occ = 1;
         if (occ * K2W_WARPS > 64) occ = 64 / K2W_WARPS;   // wscratch holds 64 warp slots per SM
+        if (L >= 6 && occ * K2W_WARPS > kK2W6MaxWarpsPerSM) occ = kK2W6MaxWarpsPerSM / K2W_WARPS;   // wscratch6 slots
     }
     uint64_t want = (P.n + K2W_WARPS - 1) / K2W_WARPS;
     uint64_t grid = (uint64_t)nsm * occ;
@@ -1049,6 +1052,11 @@ static void k2w_launch_mode(int L, const VolView& V, const Plan& P, unsigned lon
         case 4: k2w_launch_one<MODE, 4, IT>(V, P, counter, nsm, st); break;
         default: k2w_launch_one<MODE, 5, IT>(V, P, counter, nsm, st); break;
     }
+}
+static bool k2w6_disabled() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("CSVGPU_K2W6"); v = (e && strcmp(e, "0") == 0) ? 1 : 0; }
+    return v == 1;
 }
 static bool k2w_disabled() {
     static int v = -1;
@@ -1073,7 +1081,7 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
         k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
         cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
         if (e != cudaSuccess) return e;
-        cudaMemsetAsync(counter, 0, 3 * sizeof(unsigned long long), st);   // K1 items, K2w u8 / u16 bricks
+        cudaMemsetAsync(counter, 0, 4 * sizeof(unsigned long long), st);   // K1 items, K2w u8 / u16 / 64^3 bricks
     }
     if (ev) cudaEventRecord(ev[1], st);
     if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
@@ -1094,6 +1102,11 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
         size_t smem = k2_smem_bytes(Ls);
         unsigned grid = (unsigned)(P.n < 0x7fffffffull ? P.n : 0x7fffffffull);
         launch_k2_smem(mode, Ls, grid, smem, V, P, st);
+    }
+    if (V.N - min_t >= 6 && P.wscratch6 && !k2w6_disabled()) {   // 64^3 replays with <= 253 labels: K2w<6>
+        P.k2w6 = 1;
+        if (mode == OUT_RASTER) k2w_launch_one<OUT_RASTER, 6, uint8_t>(V, P, counter + 3, nsm, st);
+        else k2w_launch_one<OUT_MORTON, 6, uint8_t>(V, P, counter + 3, nsm, st);
     }
     if (V.N - min_t > 5 && gws) {
         unsigned g = (unsigned)(P.n < (uint64_t)gws_ctas ? P.n : (uint64_t)gws_ctas);

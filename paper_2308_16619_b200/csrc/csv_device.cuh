@@ -42,6 +42,8 @@ struct VolView {
     int fast_tab;              // every table count <= 4095: K1f's packed table applies
 };
 
+constexpr uint32_t kWScratch6Stride = 49152;   // K2w<6> scratch per warp slot (u16)
+constexpr int kK2W6MaxWarpsPerSM = 8;          // K2w<6> warp slots per SM
 constexpr uint32_t kWScratchStride = 4096;   // K2w scratch per warp slot (final-level parents, LMAX <= 5)
 
 // One decode call: n requests; request r decodes brick `brick[r]` at LOD lod[r].
@@ -62,6 +64,9 @@ struct Plan {
     unsigned long long* op_counts;   // K1 count mode (stats): 8 per-op totals, else nullptr
     uint16_t* wscratch;        // K2w: per resident warp, palette base per final-level active parent
     uint32_t wscratch_stride;  // u16 per warp slot
+    uint16_t* wscratch6;       // K2w<6> (64^3 replays): per warp slot kWScratch6Stride u16 =
+                               //   palette bases (32768 u16) + the final parent level (32768 u8)
+    int k2w6;                  // K2w<6> serves the u8 bricks with N - t = 6 (k2_replay<6> skips them)
 };
 
 __device__ __forceinline__ uint64_t req_local(const VolView& V, const Plan& P, uint64_t r) {

@@ -72,25 +72,22 @@ __host__ __device__ constexpr WLayout make_wlayout(int L, uint32_t isz) {
     const uint32_t R = 1u << (L - 1);
     const uint32_t ringb = 3u * (2u * R) * (2u * R) * isz;
     const uint32_t cpar = L >= 2 ? (1u << (3 * (L - 2))) : 1u;   // coarse-level parents (max)
+    const bool gfin = L >= 6;                             // final parent level in global scratch (64^3 replays)
     Y.lev = 0;
-    Y.pm = al16(wofs(L) * isz);
+    Y.pm = al16((gfin ? wofs(L - 1) : wofs(L)) * isz);
     Y.cm = al16(Y.pm + 4 * W);
     Y.wpre = al16(Y.cm + 4 * W);
     Y.ring = al16(Y.wpre + 2 * W);
     Y.plist = al16(Y.ring + ringb);
-    uint32_t end = al16(Y.plist + R * R);
+    uint32_t end = al16(Y.plist + R * R * (R > 16 ? 2u : 1u));   // u16 plane indices above 16 x 16 parents
     if (2 * R * R <= 4 * W) {
         Y.pdesc = Y.cm;                                   // cm is dead during the final sweep
     } else {
         Y.pdesc = end;
         end = al16(end + 2 * R * R);
     }
-    if (4 * cpar <= ringb) {
-        Y.clist = Y.ring;
-    } else {
-        Y.clist = end;
-        end = al16(end + 4 * cpar);
-    }
+    Y.clist = Y.ring;                                     // coarse levels: ring and plist are free
+    end = umax(end, al16(Y.ring + 4 * cpar));
     Y.cdesc = Y.clist + 2 * cpar;
     Y.spal = end;                                         // u8 mode: the brick's palette (<= 256 labels)
     if (isz == 1 && K2W_SPAL) end = al16(end + 1024);
@@ -399,11 +396,11 @@ template <typename IT>
 __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j, IT* lev, const uint32_t* pm,
                                                           uint32_t* cm, uint16_t* wpre, uint16_t* list,
                                                           uint16_t* pdesc, uint32_t& cur_c, uint32_t& ip_run,
-                                                          uint32_t& pdl, int lane) {
+                                                          uint32_t& pdl, int lane, IT* fin = nullptr) {
     const uint32_t Pn = 1u << (3 * j);
     const uint32_t W = (Pn + 31) >> 5;
     const IT* plev = lev + wofs(j);
-    IT* clev = lev + wofs(j + 1);
+    IT* clev = fin ? fin : lev + wofs(j + 1);   // fin: the final parent level lives in global scratch
     const uint32_t Mx = axis_mask(0, j), My = axis_mask(1, j), Mz = axis_mask(2, j);        // parent level
     const uint32_t Cx = axis_mask(0, j + 1), Cy = axis_mask(1, j + 1), Cz = axis_mask(2, j + 1);   // child level
     const uint32_t nact = rank_prefix(pm, W, wpre, lane);
@@ -801,14 +798,17 @@ __device__ __forceinline__ void resolve_rows(const Brick& B, uint8_t* pl, const 
 template <int MODE, int RR>
 __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const Plan& P, const uint8_t* plev,
                                                           const uint32_t* pm, uint16_t* wpre, uint8_t* ring,
-                                                          uint8_t* plist, uint32_t& cur, uint32_t& ip_run,
+                                                          uint8_t* plist_raw, uint32_t& cur, uint32_t& ip_run,
                                                           uint32_t& pdl, int lane) {
     static_assert(RR >= 4, "word-wise rows need >= 8 children per row");
+    using PLT = typename std::conditional<(RR > 16), uint16_t, uint8_t>::type;   // plane index of an active parent
+    PLT* const plist = reinterpret_cast<PLT*>(plist_raw);
+    constexpr int kFillUnroll = RR <= 16 ? 8 : 1;   // RR <= 16: Morton parts of the fill are compile-time
     constexpr uint32_t Pn = RR * RR * RR, W = (Pn + 31) / 32;
     constexpr uint32_t PP = RR * RR;           // parents per plane
     constexpr uint32_t S2 = 2 * RR;            // children (bytes) per row
     constexpr uint32_t PL = S2 * S2;           // bytes per voxel plane
-    constexpr uint32_t LG = RR == 4 ? 2 : (RR == 8 ? 3 : 4);
+    constexpr uint32_t LG = RR == 4 ? 2 : (RR == 8 ? 3 : (RR == 16 ? 4 : 5));
     constexpr uint32_t MX = 0x49249u & ((1u << (3 * LG)) - 1u), MY = MX << 1, MZ = MX << 2;
     const bool leaf = B.t == 0;
     const uint32_t nact = rank_prefix(pm, W, wpre, lane);
@@ -847,7 +847,7 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
         uint16_t* const h1 = reinterpret_cast<uint16_t*>(r1);
         // ---- fill: inactive parents' children = the parent value (ring; Morton: HBM); active list
         uint32_t nl = 0;
-#pragma unroll
+#pragma unroll kFillUnroll
         for (uint32_t i0 = 0; i0 < PP; i0 += 32) {
             const uint32_t i = i0 + lane;
             const bool ok = i < PP;
@@ -874,7 +874,7 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
                 }
             }
             const uint32_t bal = __ballot_sync(FULL, act);
-            if (act) plist[nl + __popc(bal & lanemask_lt(lane))] = (uint8_t)i;
+            if (act) plist[nl + __popc(bal & lanemask_lt(lane))] = (PLT)i;
             nl += __popc(bal);
         }
         __syncwarp();
@@ -979,9 +979,10 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         const uint64_t b = req_local(V, P, rr);
         B.t = req_lod(P, rr);
         B.N = V.N;
-        if (b >= V.nb || B.t > B.N) { if (!WIDE && lane == 0) put_result(P, rr, -1, 0, 0, 0, 0); continue; }
+        if (b >= V.nb || B.t > B.N) { if (!WIDE && LMAX <= 5 && lane == 0) put_result(P, rr, -1, 0, 0, 0, 0); continue; }
         B.n = B.N - B.t;
         if (B.t < B.N && B.n > LMAX) continue;          // served by the global-workspace kernel
+        if (LMAX == 6 && B.n != 6) continue;             // K2w<6> takes only the 64^3 replays
         B.plen = V.pal_len[b];
         if (WIDE ? B.plen <= e8::kMarkPal : B.plen > e8::kMarkPal) continue;   // the other index width's pass
         B.out_m = MODE == OUT_MORTON ? P.out + P.dst[rr] : nullptr;
@@ -1035,7 +1036,13 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         B.capc = (uint32_t)round32(limc);
         B.Ed = P.entries + eo1;
         B.capd = (uint32_t)round32(limd);
-        B.ipb = P.wscratch + (uint64_t)(blockIdx.x * K2W_WARPS + (threadIdx.x >> 5)) * P.wscratch_stride;
+        uint8_t* fin = nullptr;   // K2w<6>: the final parent level (32^3 u8) in the warp's global slot
+        if constexpr (LMAX >= 6) {
+            B.ipb = P.wscratch6 + (uint64_t)(blockIdx.x * K2W_WARPS + (threadIdx.x >> 5)) * kWScratch6Stride;
+            fin = reinterpret_cast<uint8_t*>(B.ipb + 32768);
+        } else {
+            B.ipb = P.wscratch + (uint64_t)(blockIdx.x * K2W_WARPS + (threadIdx.x >> 5)) * P.wscratch_stride;
+        }
         const bool trivial = (uint64_t)nc + nd == 0;     // relevant == 0: fill palette[0] (codec.py:353-358)
         if (lane == 0) {
             lev[0] = 0;
@@ -1047,12 +1054,14 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         uint32_t* cm = mB;
         bool failed = false;
         for (int j = 0; j + 1 < B.n; ++j) {      // parents at level N - j, children above the final level
-            const unsigned long long ek = coarse_level<IT>(B, j, lev, pm, cm, wpre, clist, cdesc, cur_c, ip_run, pdc, lane);
+            IT* const finj = (LMAX >= 6 && j + 2 == B.n) ? reinterpret_cast<IT*>(fin) : nullptr;
+            const unsigned long long ek = coarse_level<IT>(B, j, lev, pm, cm, wpre, clist, cdesc, cur_c, ip_run, pdc,
+                                                           lane, finj);
             if (ek != ~0ull) { report_error(P, rr, B.Ec, B.capc, B.src, ek, false, lane); failed = true; break; }
             uint32_t* tmp = pm; pm = cm; cm = tmp;
         }
         if (failed) continue;
-        const IT* plev = lev + wofs(B.n - 1);
+        const IT* plev = (LMAX >= 6 && B.n == 6) ? reinterpret_cast<const IT*>(fin) : lev + wofs(B.n - 1);
         // pdesc lives in whichever mask array is dead after the ping-pong (the layout aliases "cm")
         uint16_t* const fdesc = Y.pdesc == Y.cm ? reinterpret_cast<uint16_t*>(cm) : pdesc;
         uint32_t& cur = B.t == 0 ? cur_d : cur_c;
@@ -1064,7 +1073,8 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
                 case 2: ek = final_sweep<MODE, 2, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
                 case 3: ek = final_sweep8<MODE, 4>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
                 case 4: ek = final_sweep8<MODE, (LMAX >= 4 ? 8 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
-                default: ek = final_sweep8<MODE, (LMAX >= 5 ? 16 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+                case 5: ek = final_sweep8<MODE, (LMAX >= 5 ? 16 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+                default: ek = final_sweep8<MODE, (LMAX >= 6 ? 32 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
             }
         } else {
             switch (B.n) {

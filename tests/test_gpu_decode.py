@@ -364,6 +364,32 @@ print("cta ok")
     assert r.returncode == 0 and "cta ok" in r.stdout, r.stderr[-2000:]
 
 
+def test_k2w6_and_cta_replay_agree(pkg, tmp_path):
+    """64^3 replays (b = 64 at LOD 0, b = 128 at LOD 1) run on K2w<6> by default; the
+    CTA global-workspace replay (k2_replay<6>) is forced with CSVGPU_K2W6=0 in a
+    subprocess.  Both must reproduce the reference goldens at every LOD, raster and
+    Morton (the batched test covers Morton through the default path)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2308_16619_b200 as p
+from conftest import golden_bytes, golden_json, h16
+for name in ["g_b6", "j_b7"]:
+    g = golden_json("decode_%%s.json" %% name)
+    c = p.CsvContainer.from_bytes(golden_bytes(name))
+    for t in range(g["brick_log2"] + 1):
+        assert h16(p.decompress_volume(c, t)) == g["volume"][str(t)], (name, t)
+print("k2w6 ok")
+""" % (os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."),)
+    for flag in ("1", "0"):
+        env = dict(os.environ, CSVGPU_K2W6=flag, PYTHONPATH=os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "k2w6 ok" in r.stdout, (flag, r.stderr[-2000:])
+
+
 def test_side_stream_and_context_manager(pkg):
     """Decodes issued on a non-default stream allocate, launch and check on that stream;
     GpuVolume releases its device memory on leaving a `with` block."""

@@ -1,6 +1,7 @@
 """Brick size 64 (the paper's Cortex setting) vs 32 on the config-3 field:
 LOD 0 and LOD 1 full-volume decode throughput and K1 / K2 stage times (CUDA events).
-N - t = 6 (b = 64, LOD 0) runs the CTA global-workspace replay k2_replay<6>; LOD 1 and
+N - t = 6 (b = 64, LOD 0) runs K2w<6> (final parent level in global scratch; k2_replay<6>
+before, 182.7 ms -> profiles/r02_b64_before.json); LOD 1 and
 every b = 32 decode run K2w.  Output: one JSON line (also written to --out).
 
 usage: python tools/b64_probe.py [--dims 2048] [--out profiles/r02_b64.json]
@@ -51,7 +52,7 @@ def main():
                 assert torch.equal(out, vol)
             res["runs"].append({"brick": 1 << bl, "lod": t, "ms": ms[best], "gvox_s": vox / (ms[best] * 1e-3) / 1e9,
                                 "plan_k1_k2_ms": [round(x, 3) for x in stages[best]],
-                                "k2": "k2_replay<6> (CTA, global workspace)" if bl - t == 6 else "k2_warp",
+                                "k2": "k2_warp<6> (final parent level in global scratch)" if bl - t == 6 else "k2_warp<5>",
                                 "compressed_bytes": enc.payload_bytes})
             del out, r
         gv.close()
