@@ -34,9 +34,6 @@
 #ifndef K2W_RUNROLL
 #define K2W_RUNROLL 1   // u8 final level: unroll of the per-plane row loop
 #endif
-#ifndef K2W_RBRANCH
-#define K2W_RBRANCH 0   // u8 final level: branch around the z / y marker steps (0: predicated, faster)
-#endif
 constexpr int kRUnroll = K2W_RUNROLL;
 
 #ifndef K2W_SPAL
@@ -733,46 +730,62 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
 // plane read them, and (fast raster) store the labels as whole 16-byte rows.
 //   DZ = 0: even voxel plane 2pz (z markers from the previous plane `pr`),
 //   PH = 0: odd rows (no y markers), PH = 1: even rows (y from the odd row above).
+__device__ __forceinline__ uint32_t marker_bytes(uint32_t x) {   // bit 7 of every byte >= 253
+    return ((x & 0x7F7F7F7Fu) + 0x03030303u) & x & 0x80808080u;
+}
+// z / y step of one word: markers of axis (a0, a1 at bit 7) take the source word's byte
+__device__ __forceinline__ uint32_t take_bytes(uint32_t y, uint32_t m7, uint32_t src) {
+    const uint32_t M = (m7 >> 7) * 0xFFu;
+    return (y & ~M) | (src & M);
+}
+
 template <int RR, int DZ, int PH>
 __device__ __forceinline__ void resolve_rows(const Brick& B, uint8_t* pl, const uint8_t* pr, bool fast, uint32_t* zb,
                                              int lane) {
     static_assert(K2W_SPAL, "the u8 pass reads labels from the shared palette copy");
-    constexpr uint32_t S2 = 2 * RR, WPR = S2 / 4, HW = RR * RR / 2, RPI = 32 / WPR;   // row pairs per iteration
+    // one lane = 8 children (two words) of a row; RPI row pairs per warp iteration
+    constexpr uint32_t S2 = 2 * RR, WPR = S2 / 8, HW = RR * RR / 4, RPI = 32 / WPR;
     const uint32_t rp0 = lane / WPR, cw = lane % WPR;
     const uint32_t row0 = 2 * rp0 + (PH ? 0u : 1u);
-    uint32_t* wp = reinterpret_cast<uint32_t*>(pl + row0 * S2) + cw;
-    const uint32_t* pw = reinterpret_cast<const uint32_t*>(pr + row0 * S2) + cw;
-    uint32_t* op = fast ? zb + row0 * B.pitch + 4 * cw : nullptr;
+    uint2* wp = reinterpret_cast<uint2*>(pl + row0 * S2) + cw;
+    const uint2* pw = reinterpret_cast<const uint2*>(pr + row0 * S2) + cw;
+    uint32_t* op = fast ? zb + row0 * B.pitch + 8 * cw : nullptr;
     const uint8_t* const lab = reinterpret_cast<const uint8_t*>(B.spal);
     // write-back needed unless nothing reads these words again (even rows of the even plane, fast raster)
     const bool keep = !(DZ == 0 && PH == 1) || !fast;
 #pragma unroll kRUnroll
     for (uint32_t w0 = 0; w0 < HW; w0 += 32) {
         const bool okw = HW >= 32 || lane < (int)HW;
-        const uint32_t x = okw ? *wp : 0u;
-        const uint32_t f = ((x & 0x7F7F7F7Fu) + 0x03030303u) & x & 0x80808080u;   // marker bytes (>= 253)
-        const uint32_t a0 = x << 7, a1 = x << 6;                                 // axis bits at bit 7
-        uint32_t y = x;
-        if (!K2W_RBRANCH || f) {
-            if (DZ == 0) {   // z: the previous voxel plane (final)
-                const uint32_t M = ((f & a0 & a1) >> 7) * 0xFFu;
-                if (!K2W_RBRANCH || M) y = (y & ~M) | ((okw ? *pw : 0u) & M);
-            }
-            if (PH == 1) {   // y: the odd row above (resolved in phase 0)
-                const uint32_t M = ((f & ~a0 & a1) >> 7) * 0xFFu;
-                if (!K2W_RBRANCH || M) y = (y & ~M) | ((okw ? *(wp - WPR) : 0u) & M);
-            }
+        const uint2 x = okw ? *wp : make_uint2(0u, 0u);
+        const uint32_t f0 = marker_bytes(x.x), f1 = marker_bytes(x.y);
+        const uint32_t a00 = x.x << 7, a01 = x.x << 6, a10 = x.y << 7, a11 = x.y << 6;   // axis bits at bit 7
+        uint32_t y0 = x.x, y1 = x.y;
+        if (DZ == 0) {   // z: the previous voxel plane (final)
+            const uint2 z = okw ? *pw : make_uint2(0u, 0u);
+            y0 = take_bytes(y0, f0 & a00 & a01, z.x);
+            y1 = take_bytes(y1, f1 & a10 & a11, z.y);
         }
-        const uint32_t left = __shfl_up_sync(FULL, y, 1);                         // x: the byte to the left
-        const uint32_t Mx = ((f & a0 & ~a1) >> 7) * 0xFFu;
-        y = (y & ~Mx) | (__byte_perm(y, left, 0x2107) & Mx);
-        if (keep && f) *wp = y;
+        if (PH == 1) {   // y: the odd row above (resolved in phase 0)
+            const uint2 u = okw ? *(wp - WPR) : make_uint2(0u, 0u);
+            y0 = take_bytes(y0, f0 & ~a00 & a01, u.x);
+            y1 = take_bytes(y1, f1 & ~a10 & a11, u.y);
+        }
+        // x: the byte to the left (word 0's byte 0 from the left lane's word 1; odd-x sources are final)
+        const uint32_t left = __shfl_up_sync(FULL, y1, 1);
+        y0 = take_bytes(y0, f0 & a00 & ~a01, __byte_perm(y0, left, 0x2107));
+        y1 = take_bytes(y1, f1 & a10 & ~a11, __byte_perm(y1, y0, 0x2107));
+        if (keep && (f0 | f1)) *wp = make_uint2(y0, y1);
         if (fast && okw) {
-            const uint4 v = make_uint4(*reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y, 0, 0x4440)),
-                                       *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y, 0, 0x4441)),
-                                       *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y, 0, 0x4442)),
-                                       *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y, 0, 0x4443)));
-            __stcs(reinterpret_cast<uint4*>(op), v);   // evict-first
+            const uint4 v0 = make_uint4(*reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y0, 0, 0x4440)),
+                                        *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y0, 0, 0x4441)),
+                                        *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y0, 0, 0x4442)),
+                                        *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y0, 0, 0x4443)));
+            const uint4 v1 = make_uint4(*reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y1, 0, 0x4440)),
+                                        *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y1, 0, 0x4441)),
+                                        *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y1, 0, 0x4442)),
+                                        *reinterpret_cast<const uint32_t*>(lab + 4 * __byte_perm(y1, 0, 0x4443)));
+            __stcs(reinterpret_cast<uint4*>(op), v0);   // evict-first
+            __stcs(reinterpret_cast<uint4*>(op) + 1, v1);
             op += 2 * RPI * B.pitch;
         }
         wp += 2 * RPI * WPR;
