@@ -849,7 +849,7 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
     }
     __syncwarp();
     const bool fast = MODE == OUT_RASTER && B.al16r;
-    const uint32_t qlane = spread3_u32(lane % RR) | (spread3_u32((lane / RR) % RR) << 1);
+    const uint32_t qlane = spread3_u32(2 * (lane % (RR / 2))) | (spread3_u32((lane / (RR / 2)) % RR) << 1);
 #pragma unroll 1
     for (uint32_t pz = 0; pz < RR; ++pz) {
         const uint32_t sz = spread3_u32(pz) << 2;
@@ -858,37 +858,48 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
         const uint8_t* const pr = ring + ((2 * pz + 2) % 3) * PL;   // voxel plane 2pz-1 (final)
         uint16_t* const h0 = reinterpret_cast<uint16_t*>(r0);
         uint16_t* const h1 = reinterpret_cast<uint16_t*>(r1);
-        // ---- fill: inactive parents' children = the parent value (ring; Morton: HBM); active list
+        // ---- fill: every parent's children = the parent value (ring; Morton: inactive ones to HBM),
+        // two x-adjacent parents per lane (Morton codes q, q | 1: one u16 load, one u32 store per row);
+        // active parents are listed (and overwritten by the active pass)
         uint32_t nl = 0;
 #pragma unroll kFillUnroll
-        for (uint32_t i0 = 0; i0 < PP; i0 += 32) {
-            const uint32_t i = i0 + lane;
-            const bool ok = i < PP;
-            const uint32_t px = i % RR, py = i / RR;
-            // i0 / RR and lane / RR have disjoint bits: the Morton code splits into a
-            // per-lane part and a compile-time part of this (unrolled) iteration
-            const uint32_t q = qlane | (spread3_c(i0 / RR) << 1) | sz;
-            uint32_t mw = 0, pv = 0;
+        for (uint32_t i0 = 0; i0 < PP / 2; i0 += 32) {
+            const uint32_t j = i0 + lane;
+            const bool ok = j < PP / 2;
+            const uint32_t px = 2 * (j % (RR / 2)), py = j / (RR / 2);
+            // i0 / (RR/2) and lane / (RR/2) have disjoint bits: the Morton code splits into a
+            // per-lane part and a (compile-time when unrolled) part of this iteration
+            const uint32_t q = qlane | (spread3_c(i0 / (RR / 2)) << 1) | sz;
+            uint32_t mw = 0, pv2 = 0;
             if (ok) {
-                pv = plev[q];
-                mw = pm[q >> 5];
+                pv2 = *reinterpret_cast<const uint16_t*>(plev + q);   // parents q and q | 1
+                mw = pm[q >> 5] >> (q & 31);
             }
-            const bool act = ok && ((mw >> (q & 31)) & 1u);
-            if (ok && !act) {
-                const uint16_t pp = (uint16_t)(pv * 0x0101u);
-                h0[(2 * py) * RR + px] = pp;
-                h0[(2 * py + 1) * RR + px] = pp;
-                h1[(2 * py) * RR + px] = pp;
-                h1[(2 * py + 1) * RR + px] = pp;
+            const bool act0 = ok && (mw & 1u), act1 = ok && (mw & 2u);
+            if (ok) {
+                const uint32_t pp = (pv2 & 0xFFu) * 0x0101u | (pv2 >> 8) * 0x01010000u;
+                uint32_t* const w0 = reinterpret_cast<uint32_t*>(r0 + (2 * py) * S2 + 2 * px);
+                uint32_t* const w1 = reinterpret_cast<uint32_t*>(r1 + (2 * py) * S2 + 2 * px);
+                w0[0] = pp;
+                w0[S2 / 4] = pp;
+                w1[0] = pp;
+                w1[S2 / 4] = pp;
                 if (MODE == OUT_MORTON) {
-                    const uint32_t l = label_of<uint8_t>(B, pv);
-                    const uint32_t lab[8] = {l, l, l, l, l, l, l, l};
-                    store_children<MODE>(B, P, q, px, py, pz, lab);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h ? act1 : act0) continue;
+                        const uint32_t l = label_of<uint8_t>(B, h ? pv2 >> 8 : pv2 & 0xFFu);
+                        const uint32_t lab[8] = {l, l, l, l, l, l, l, l};
+                        store_children<MODE>(B, P, q | (uint32_t)h, px + h, py, pz, lab);
+                    }
                 }
             }
-            const uint32_t bal = __ballot_sync(FULL, act);
-            if (act) plist[nl + __popc(bal & lanemask_lt(lane))] = (PLT)i;
-            nl += __popc(bal);
+            const uint32_t bal0 = __ballot_sync(FULL, act0), bal1 = __ballot_sync(FULL, act1);
+            const uint32_t lt = lanemask_lt(lane);
+            const uint32_t i = py * RR + px;
+            if (act0) plist[nl + __popc(bal0 & lt)] = (PLT)i;
+            if (act1) plist[nl + __popc(bal0) + __popc(bal1 & lt)] = (PLT)(i + 1);
+            nl += __popc(bal0) + __popc(bal1);
         }
         __syncwarp();
         // ---- active parents: one lane each, SWAR evaluation, pending children as markers
