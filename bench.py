@@ -597,7 +597,7 @@ def run_ours(args, world, rank, local):
                 "traffic": traffic.get(name), "peak_kind": peak_kind, "algorithmic_bytes": kbytes, "kernel_ms": kms}
     kernels = {"k1_streams": kline("k1_streams", k1_ms, k1_bytes), "k2_warp": kline("k2_warp", k2_ms, k2_bytes)}
     roofline = dict(kernels["k2_warp"] if k2_ms >= k1_ms else kernels["k1_streams"])
-    long_pal = int(d["palette_len"].max()) > 256 if n_b else False      # K2w runs a second (u16) pass
+    long_pal = int(d["palette_len"].max()) > 253 if n_b else False      # K2w runs a second (u16) pass (e8::kMarkPal)
     step_gbs = step_bytes / (ms_rank * 1e-3) / 1e9
     line = {
         "metric": "decoded GVoxel/s (full-volume decode, LOD 0)", "value": value, "unit": "GVoxel/s",

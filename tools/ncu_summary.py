@@ -64,7 +64,7 @@ def main():
             for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 v, u = row[m]
                 byt += float(v.replace(",", "")) * SCALE.get(u, 1.0)
-            key = "k2_replay" if "k2_" in name else ("k1_streams" if "k1_" in name else name)
+            key = "k2_warp" if "k2_" in name else ("k1_streams" if "k1_" in name else name)
             traffic.setdefault(key, byt)
     with open(out_txt, "w") as f:
         f.write("\n".join(lines))

@@ -1,6 +1,7 @@
 """Small decode workload for compute-sanitizer runs (memcheck / racecheck / synccheck):
 config-1 container at LOD 0 and 2 (raster, K2w u8 pass), a batched Morton decode with
-mixed LODs, a b=64 container (global-workspace kernel), stats() (K1 count mode), a
+mixed LODs, b=64 / b=128 containers (K2w<6>, k2_replay<7>), the per-brick resident path,
+the rANS / pyramid drop-ins, stats() (K1 count mode), a
 noise container whose palettes need the u16 K2w pass, and one device-cache frame with
 LOD selection, visibility and cold-detail staging."""
 import os
@@ -27,7 +28,18 @@ pool = torch.empty(int(sizes.sum()), dtype=torch.int32, device="cuda")
 p.GpuVolume.raise_first(vol.decode_bricks(bricks, lods, dst, pool), 64)
 with open(os.path.join(G, "vol_g_b6.csv1"), "rb") as f:
     g = p.CsvContainer.from_bytes(f.read())
-p.decompress_volume(g, 0)
+p.decompress_volume(g, 0)                       # b=64 LOD 0: K2w<6>
+with open(os.path.join(G, "vol_j_b7.csv1"), "rb") as f:
+    j = p.CsvContainer.from_bytes(f.read())
+p.decompress_volume(j, 0)                       # b=128 LOD 0: k2_replay<7>
+p.decompress_volume(j, 1)                       # b=128 LOD 1: K2w<6>
+for t in (0, 1, 3):                             # per-brick path on the resident container
+    c.decode_brick(5, t)
+tab = c.tables.leaf                             # stand-alone drop-ins
+nib = np.arange(300, dtype=np.uint8) % 16
+assert np.array_equal(p.rans_decode(p.rans_encode(nib, tab), 300, tab), nib)
+pyr = p.build_pyramid(np.arange(4096, dtype=np.uint32) % 7, p.BrickConfig(4))
+p.downsample_level(np.arange(512, dtype=np.uint32).reshape(8, 8, 8) % 5)
 s = p.stats(p.CsvContainer.from_bytes(open(os.path.join(G, "vol_d_b5_mem.csv1"), "rb").read()))
 k = p.CsvContainer.from_bytes(open(os.path.join(G, "vol_k_b5_noise_raw.csv1"), "rb").read())
 p.decompress_volume(k, 0)
