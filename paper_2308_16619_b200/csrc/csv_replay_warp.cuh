@@ -440,7 +440,7 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
             cmb[q] = (uint8_t)(((~(w >> 3) & ONES) * 0x0102040810204080ull) >> 56);   // no stop: visited next level
             if constexpr (sizeof(IT) == 1) {
                 e8::Out g;
-                e8::eval8(w, pv, pxp, pyp, pzp, bf, ipq, B.plen, vmask, false, g);
+                e8::eval8<true>(w, pv, pxp, pyp, pzp, bf, ipq, B.plen, vmask, false, g);   // pending: markers
                 *reinterpret_cast<uint2*>(clev + 8 * q) = make_uint2(g.vlo, g.vhi);
                 pdesc[k] = (uint16_t)g.pend;
                 anyp |= g.pend;
@@ -463,7 +463,40 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
         }
     }
     __syncwarp();
-    if (__any_sync(FULL, anyp != 0u)) {
+    if (sizeof(IT) == 1 && __any_sync(FULL, anyp != 0u)) {
+        // u8: one pass.  A pending child holds the marker 252 + axis; it copies the -1
+        // neighbour on that axis (codec.py:422-423), following markers (at most three hops,
+        // each adds an odd coordinate) until a final value.  The warp reads first and the
+        // parents' 8-child words are rewritten after a __syncwarp.
+#pragma unroll 1
+        for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            uint32_t m = k < nact ? (uint32_t)pdesc[k] : 0u;
+            const uint32_t q = m ? list[k] : 0u;
+            uint32_t nlo = 0, nhi = 0, mlo = 0, mhi = 0;
+            while (m) {
+                const uint32_t c = (uint32_t)(__ffs(m) - 1) >> 1;
+                uint32_t a = (m >> (2 * c)) & 3u;
+                m &= ~(3u << (2 * c));
+                uint32_t src = (q << 3) | c, v;
+#pragma unroll 1
+                do {
+                    src = morton_dec(src, a == 1u ? Cx : (a == 2u ? Cy : Cz));
+                    v = clev[src];
+                    a = v - 252u;
+                } while (v >= 253u);
+                if (c < 4) { nlo |= v << (8 * c); mlo |= 0xFFu << (8 * c); }
+                else { nhi |= v << (8 * (c - 4)); mhi |= 0xFFu << (8 * (c - 4)); }
+            }
+            __syncwarp();
+            if (mlo | mhi) {
+                uint2* const p = reinterpret_cast<uint2*>(clev + 8 * q);
+                const uint2 o = *p;
+                *p = make_uint2((o.x & ~mlo) | nlo, (o.y & ~mhi) | nhi);
+            }
+            __syncwarp();
+        }
+    } else if (__any_sync(FULL, anyp != 0u)) {
         // rounds by decreasing popcount of the child index: targets are final
 #pragma unroll 1
         for (int rd = 0; rd < 3; ++rd) {
