@@ -368,14 +368,18 @@ def desired_lods(grid, b, cam, fov, height, max_lod):
 
 
 # ---------------------------------------------------------------------------- config 5
-def timeseries_leg(p, torch, dev, stream, steps: int = 2, dims=(1024, 1024, 1024), cells: int = 22):
-    """1024^3 Voronoi timesteps (seed 3, seeds drifting
-    by <= k voxels at step k); per timestep GPU encode then GPU decode, both
-    timed with CUDA events (the decode after one untimed call that allocates the
-    new volume's workspace); lossless round trip checked (untimed)."""
+def timeseries_leg(p, torch, dev, stream, world: int = 1, rank: int = 0, total: int = 16,
+                   dims=(1024, 1024, 1024), cells: int = 22):
+    """16 timesteps of 1024^3 Voronoi (seed 3, seeds drifting
+    by <= k voxels at step k) sharded over the ranks (rank r takes timesteps r, r + N, ...;
+    2 per rank at N = 8, 16 on one GPU); per timestep GPU encode then GPU decode, both
+    timed with CUDA events (the decode after one untimed call that allocates the new
+    volume's workspace); lossless round trip checked (untimed).  Ensemble throughput =
+    16 * 1024^3 voxels / the slowest rank's summed encode (decode) time."""
     enc_ms, dec_ms = [], []
     X, Y, Z = dims
-    for k in range(steps):
+    mine = list(range(rank, total, world))
+    for k in mine:
         vol = p.synth_voronoi(dims, cells, seed=3, membrane=False, drift=float(min(k, 16)), drift_seed=3 + k,
                               device=dev)
         torch.cuda.synchronize()
@@ -399,11 +403,15 @@ def timeseries_leg(p, torch, dev, stream, steps: int = 2, dims=(1024, 1024, 1024
         enc.close()
         del vol, out
         torch.cuda.empty_cache()
-    vox = X * Y * Z * steps
-    te, td = sum(enc_ms) / 1e3, sum(dec_ms) / 1e3
-    return {"timesteps": steps, "dims": list(dims), "encode_gvox_s": vox / te / 1e9, "decode_gvox_s": vox / td / 1e9,
-            "roundtrip_gvox_s": vox / (te + td) / 1e9, "encode_ms": enc_ms, "decode_ms": dec_ms,
-            "workload": "config 5 share of one GPU: 2 of 16 timesteps of 1024^3 Voronoi (22^3 cells, seed 3, drift <= k)"}
+    te = max_over_ranks(sum(enc_ms) / 1e3, world)
+    td = max_over_ranks(sum(dec_ms) / 1e3, world)
+    vox = X * Y * Z * total
+    return {"timesteps": total, "per_rank": len(mine), "dims": list(dims), "encode_gvox_s": vox / te / 1e9,
+            "decode_gvox_s": vox / td / 1e9, "roundtrip_gvox_s": vox / (te + td) / 1e9,
+            "encode_ms_rank0": [round(x, 2) for x in enc_ms], "decode_ms_rank0": [round(x, 3) for x in dec_ms],
+            "workload": f"config 5: {total} timesteps of 1024^3 Voronoi (22^3 cells, seed 3, drift <= k) over "
+                        f"{world} GPU(s), rank r takes timesteps r, r + N, ...; max over ranks of the summed "
+                        "CUDA-event times"}
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -625,11 +633,13 @@ def run_ours(args, world, rank, local):
         line["decode_gather"] = gather
     # ---- config 4: batched random-access decode into a device brick pool
     cache_reqs = None
-    if not args.no_cache and not args.profile and world == 1:
+    if not args.no_cache and not args.profile and (world == 1 or not weak):
         lod, dist = desired_lods((gx, gy, gz), b, (1024.0, 1024.0, -64.0), math.pi / 3, 1080, BRICK_LOG2)
         order = np.argsort(dist, kind="stable")[:65536]
         reqs = [(int(i), int(lod[i])) for i in order if lod[i] < BRICK_LOG2]
         cache_reqs = reqs
+        if world > 1:   # strong: each rank serves the requests of the bricks it owns (no collective)
+            reqs = [r for r in reqs if brick_range[0] <= r[0] < brick_range[1]]
         cache = p.BrickCache(gx * gy * gz, BRICK_LOG2, pool_bytes=8 << 30, device=dev)
         cache.begin_frame()
         for br, l in reqs:
@@ -641,26 +651,36 @@ def run_ours(args, world, rank, local):
         bricks = torch.from_numpy(arr[:, 0].astype(np.int32)).to(dev)
         lods = torch.from_numpy(arr[:, 1].astype(np.uint8)).to(dev)
         dst = torch.from_numpy(arr[:, 2] * 8).to(dev)
-        fvol = enc.to_volume()
-        cres = torch.empty((len(live), 4), dtype=torch.int64, device=dev)
+        fvol = enc.to_volume() if world == 1 else gv
+        cres = torch.empty((max(len(live), 1), 4), dtype=torch.int64, device=dev)
         for _ in range(args.warmup):
             fvol.decode_bricks(bricks, lods, dst, cache.pool, results=cres)
         torch.cuda.synchronize()
         p.GpuVolume.raise_first(cres, len(live))
+        barrier(world)
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
             fvol.decode_bricks(bricks, lods, dst, cache.pool, results=cres)
         e1.record(stream)
         torch.cuda.synchronize()
-        cms = e0.elapsed_time(e1) / args.steps
-        cvox = int(sum(8 ** (BRICK_LOG2 - int(l)) for l in arr[:, 1]))
-        n0 = int((arr[:, 1] == 0).sum())
+        barrier(world)
+        cms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        cvox = sum_over_ranks(int(sum(8 ** (BRICK_LOG2 - int(l)) for l in arr[:, 1])) if len(arr) else 0, world)
+        n0 = sum_over_ranks(int((arr[:, 1] == 0).sum()) if len(arr) else 0, world)
+        nreq = sum_over_ranks(len(live), world)
         line["random_brick"] = {"value": cvox / (cms * 1e-3) / 1e9, "unit": "GVoxel/s", "ms_per_step": cms,
-                                "requests": len(live), "lod0": n0, "lod1": len(live) - n0, "voxels": cvox,
+                                "requests": nreq, "lod0": n0, "lod1": nreq - n0, "voxels": cvox,
                                 "workload": "config 4: camera (1024,1024,-64) +z, H=1080, fov pi/3, "
                                             "desired_lods, 65,536 nearest bricks -> BrickCache plan -> one "
-                                            "csv_decode_bricks batch into an 8 GiB device pool"}
+                                            "csv_decode_bricks batch into an 8 GiB device pool"
+                                            + (f"; requests partitioned by brick owner over {world} ranks, "
+                                               "max-over-ranks time" if world > 1 else "")}
+        if world > 1:
+            del cache
+            torch.cuda.empty_cache()
+    if cache_reqs is not None and world == 1:
         # the same frame with the residency bookkeeping on the GPU too:
         # device LOD selection + DeviceBrickCache (evict / free stacks / carve, atomics) + batched decode
         del cache
@@ -733,9 +753,9 @@ def run_ours(args, world, rank, local):
         cold.close()
         dcache.close()
         fvol.close()
-    # ---- config 5: time series encode + decode (2 timesteps = one GPU's share of 16 over 8 GPUs)
-    if not args.no_cache and not args.profile and world == 1 and args.workload == "config3" and not args.zlayers:
-        line["timeseries"] = timeseries_leg(p, torch, dev, stream)
+    # ---- config 5: the 16-timestep ensemble encode + decode, timesteps sharded over the ranks
+    if not args.no_cache and not args.profile and args.workload == "config3" and not args.zlayers:
+        line["timeseries"] = timeseries_leg(p, torch, dev, stream, world, rank)
     # ---- e2e: public API, host buffers in, host volume out (pinned)
     if not args.no_e2e and not args.profile:
         try:                                   # one pinned 34 GB volume per rank; pageable if the host refuses
