@@ -344,7 +344,14 @@ __global__ void __launch_bounds__(E_THREADS) e12_bricks(EncView E) {
 }
 
 // E3: one lane per stream, reverse rANS (rans.py:120-137) or nibble packing (container.py:340-345).
-struct EncTables { uint32_t freq[2][16]; uint32_t cum[2][17]; };
+// Per symbol: the reciprocal form of x -> (x / f) * 4096 + x % f + cum (rans.py:133): with
+// q = umulhi(x, rcp) >> rsh = x / f (exact for 2^15 <= x < 2^31), the state update is
+// x + bias + q * (4096 - f) -- no integer division in the lane's loop.  f = 1 uses
+// rcp = ~0, rsh = 0, bias = cum + 4095 (q = x - 1).
+struct EncTables {
+    uint32_t freq[2][16]; uint32_t cum[2][17];
+    uint32_t rcp[2][16], rsh[2][16], bias[2][16], cmpl[2][16];
+};
 
 __global__ void __launch_bounds__(256) e3_streams(EncView E, EncTables T, int entropy, uint32_t enc_doff) {
     uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -374,7 +381,8 @@ __global__ void __launch_bounds__(256) e3_streams(EncView E, EncTables T, int en
                 uint32_t f = T.freq[s][sy];
                 uint32_t xmax = ((kStateLower >> kPrecision) << 8) * f;
                 while (x >= xmax) { slot[--ptr] = (uint8_t)(x & 0xFF); x >>= 8; }
-                x = ((x / f) << kPrecision) + (x % f) + T.cum[s][sy];
+                const uint32_t q = __umulhi(x, T.rcp[s][sy]) >> T.rsh[s][sy];
+                x = x + T.bias[s][sy] + q * T.cmpl[s][sy];
             }
         }
         slot[--ptr] = (uint8_t)(x >> 24);
@@ -652,7 +660,10 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
     size_t freeb = 0, totb = 0;
     cudaMemGetInfo(&freeb, &totb);
     mark("meminfo", 0);
-    uint64_t budget = std::min<uint64_t>((uint64_t)(freeb * 0.35), 2ull << 30);
+    // chunk scratch budget (grow-only arena): CSVGPU_ENC_BUDGET_GB overrides the default
+    // (8 GB: a 1024^3 volume of 32^3 bricks encodes in 2 chunks, 16.4 ms; 2 GB: 8 chunks, 25.5 ms)
+    static const double budget_gb = std::getenv("CSVGPU_ENC_BUDGET_GB") ? std::atof(std::getenv("CSVGPU_ENC_BUDGET_GB")) : 8.0;
+    uint64_t budget = std::min<uint64_t>((uint64_t)(freeb * 0.35), (uint64_t)(budget_gb * (1ull << 30)));
     uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, budget / per_brick));
     chunk = std::min<uint64_t>(chunk, 65536);
 
@@ -725,6 +736,19 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
         const uint16_t* cn = tb ? lcnt : icnt;
         T.cum[tb][0] = 0;
         for (int s = 0; s < 16; ++s) { T.freq[tb][s] = cn[s]; T.cum[tb][s + 1] = T.cum[tb][s] + cn[s]; }
+        for (int s = 0; s < 16; ++s) {
+            const uint32_t f = T.freq[tb][s];
+            T.cmpl[tb][s] = kTotalFreq - f;
+            if (f < 2) {
+                T.rcp[tb][s] = 0xFFFFFFFFu; T.rsh[tb][s] = 0; T.bias[tb][s] = T.cum[tb][s] + kTotalFreq - 1;
+            } else {
+                uint32_t sh = 0;
+                while (f > (1u << sh)) ++sh;
+                T.rcp[tb][s] = (uint32_t)(((1ull << (sh + 31)) + f - 1) / f);
+                T.rsh[tb][s] = sh - 1;
+                T.bias[tb][s] = T.cum[tb][s];
+            }
+        }
     }
     // ---- main pass, chunk by chunk
     uint64_t pos[3] = {0, 0, 0};
