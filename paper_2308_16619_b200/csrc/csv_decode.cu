@@ -375,6 +375,7 @@ __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t
 // longest lane's chain (latency): 9.5 vs 10.6 ms on config 3, 1.12 vs 1.17 ms on config 2.
 constexpr int K1_MINB_THROUGHPUT = 5;
 constexpr int K1_MINB_LATENCY = 3;
+constexpr uint64_t kK1TinyBlocks = 8;   // plans of <= 8 K1 blocks (<= 1024 requests) use the latency-optimised steps
 template <bool ENTROPY, bool COUNT, int MINB>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_streams(VolView V, Plan P, unsigned long long* counter) {
     __shared__ uint32_t tab[2 * 4096];
@@ -949,20 +950,20 @@ static void launch_k1_variant(const VolView& V, const Plan& P, unsigned long lon
     k1_streams<E, COUNT, MINB><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
 }
 
-template <int MINB>
+template <int MINB, bool LAT = false>
 static void launch_k1f_variant(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, uint64_t blocks,
                                cudaStream_t st) {
     static int per_sm = 0;
     if (per_sm == 0) {
         int b = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_fast<MINB>, K1_THREADS, 0) != cudaSuccess || b < 1)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_fast<MINB, LAT>, K1_THREADS, 0) != cudaSuccess || b < 1)
             b = MINB;
         per_sm = b;
     }
     const uint64_t cap = (uint64_t)nsm * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k1_fast<MINB><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
+    k1_fast<MINB, LAT><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
 }
 
 static bool k1_old() {
@@ -978,7 +979,8 @@ static void launch_k1(const VolView& V, const Plan& P, unsigned long long* count
     const uint64_t blocks = (want + K1_THREADS / 32 - 1) / (K1_THREADS / 32);
     if (E && !COUNT && V.fast_tab && !k1_old()) {
         if (blocks > (uint64_t)nsm * K1_MINB_LATENCY) launch_k1f_variant<K1_MINB_THROUGHPUT>(V, P, counter, nsm, blocks, st);
-        else launch_k1f_variant<K1_MINB_LATENCY>(V, P, counter, nsm, blocks, st);
+        else if (blocks > kK1TinyBlocks) launch_k1f_variant<K1_MINB_LATENCY>(V, P, counter, nsm, blocks, st);
+        else launch_k1f_variant<K1_MINB_LATENCY, true>(V, P, counter, nsm, blocks, st);   // per-brick calls
         return;
     }
     if (blocks > (uint64_t)nsm * K1_MINB_LATENCY)      // more than one wave of the latency variant

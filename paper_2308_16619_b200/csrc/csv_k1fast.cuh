@@ -114,8 +114,40 @@ __device__ __forceinline__ uint32_t fl_lookup(const FLane& L) {
     return e;
 }
 
+// LAT (the single-wave variant, where the longest stream's chain sets the time): the
+// renormalisation is taken from three candidates chosen by two compares instead of
+// count-leading-zeros -> shift amount -> funnel shift, and the table address is one
+// AND + one multiply-add; fewer cycles on the symbol-to-symbol dependency chain, a few
+// more ALU instructions.
+template <bool LAT = false>
+__device__ __forceinline__ uint32_t fl_lookup_t(const FLane& L) {
+    uint32_t e;
+    if (LAT) {
+        uint32_t a;
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a) : "r"(L.x & (kTotalFreq - 1u)), "r"(L.tb));
+        asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(a));
+    } else {
+        e = fl_lookup(L);
+    }
+    return e;
+}
+
+template <bool LAT = false>
 __device__ __forceinline__ void fl_step_fast(FLane& L) {
-    const uint32_t e = fl_lookup(L);
+    const uint32_t e = fl_lookup_t<LAT>(L);
+    if (LAT) {
+        const uint32_t f = __umulhi(e, 1u << 12), g = __umulhi(e, 1u << 24);
+        const uint32_t xn = f * (__umulhi(L.x, 1u << 20) - 4096u) + g;
+        const bool r1 = xn < kStateLower, r2 = xn < (1u << 15);   // 1 / 2 renormalisation bytes
+        const uint32_t x8 = __funnelshift_l(L.hi, xn, 8u), x16 = __funnelshift_l(L.hi, xn, 16u);
+        const uint32_t s8 = r2 ? 16u : (r1 ? 8u : 0u);
+        L.x = r2 ? x16 : (r1 ? x8 : xn);
+        L.hi = __funnelshift_l(L.lo, L.hi, s8);
+        L.lo <<= s8;
+        L.nb -= (int)s8;
+        fl_emit(L, e);
+        return;
+    }
 #if K1F_FMA_DECODE
     // the same xn with the field extractions on the FMA pipe (the ALU pipe is the bottleneck):
     // e >> 8 = f << 12 | bias, so xn = f * ((x >> 12) - 4096) + (e >> 8) (mod 2^32)
@@ -243,8 +275,9 @@ __device__ bool fl_init(FLane& L, const VolView& V, const Plan& P, uint64_t item
     return true;
 }
 
-template <int MINB>
+template <int MINB, bool LAT>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_fast(VolView V, Plan P, unsigned long long* counter) {
+    // LAT: plans of a few blocks (per-brick calls), where one lane's chain is the whole time
     __shared__ uint32_t tab[2 * 4096];
     __shared__ __align__(32) uint2 ring[K1_THREADS][4];
     for (int i = threadIdx.x; i < 2 * 4096; i += blockDim.x) {
@@ -280,8 +313,8 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_fast(VolView V, Plan P, u
 #pragma unroll
                 for (int u = 0; u < K1F_BLOCK / 2; ++u) {
                     if (L.nb < 32) fl_refill(L);
-                    fl_step_fast(L);
-                    fl_step_fast(L);
+                    fl_step_fast<LAT>(L);
+                    fl_step_fast<LAT>(L);
                     if ((u & 3) == 3) fl_flush(L);   // <= 8 entries between flushes: the ring never overflows
                 }
                 L.i += K1F_BLOCK;
