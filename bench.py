@@ -570,6 +570,40 @@ def run_ours(args, world, rank, local):
             if mode == "all" and world > 1 and not root:
                 del vol_all
                 torch.cuda.empty_cache()
+        # fused decode + gather through peer memory (distributed.PeerVolume): the root's volume
+        # is mapped by every rank (CUDA IPC; NVLink P2P across GPUs) and each rank's K2w stores
+        # its rows straight into it -- the transfer overlaps the decode, no NCCL data movement
+        from paper_2308_16619_b200.distributed import PeerVolume
+        if root:
+            pv = PeerVolume.alloc((Z, Y, X), dev)
+        if world > 1:
+            import torch.distributed as tdist
+            box = [pv.handle if root else None]
+            tdist.broadcast_object_list(box, src=0)
+            if not root:
+                pv = PeerVolume.open(box[0], (Z, Y, X), dev)
+        pptr = pv.rows_ptr(zr[0])
+        gv.decode_into(0, pptr, zr, res)
+        torch.cuda.synchronize()
+        barrier(world)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            gv.decode_into(0, pptr, zr, res)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        gms = max_over_ranks(g0.elapsed_time(g1) / args.steps, world)
+        ent = {"value": X * Y * Z / (gms * 1e-3) / 1e9, "unit": "GVoxel/s", "ms_per_step": gms,
+               "gather_bytes_per_rank": 0 if root else 4 * voxels_rank,
+               "collective": ("none (N = 1): decode into an IPC-shareable volume" if world == 1 else
+                              "none: every rank's K2w stores its rows into the root's volume through CUDA IPC "
+                              "peer memory (NVLink P2P); max-over-ranks decode time with the stores landed")}
+        if root:
+            ent["check"] = check_bricks(blocks, pv.tensor(), 0, 0, gx * gy * gz, grid)
+        gather["peer"] = ent
+        pv.close()
+        del pv
     # ---- per-stage timing (CUDA events on the launching stream, separate pass)
     gv.set_timing(True)
     stages = []

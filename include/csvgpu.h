@@ -255,6 +255,18 @@ int csv_build_pyramid(const uint32_t* d_labels, uint64_t n_bricks, int brick_log
  * (nz/2, ny/2, nx/2), mode of each 2x2x2 cell with first-occurrence ties. */
 int csv_downsample(const uint32_t* d_in, int64_t nz, int64_t ny, int64_t nx, uint32_t* d_out, uintptr_t stream);
 
+/* ---------------------------------------------------------------- fused decode + gather
+ * The receiving rank allocates the decoded volume as an IPC-shareable buffer and
+ * publishes the 64-byte handle; the other ranks map it (NVLink peer memory on a
+ * multi-GPU node) and pass pointers INSIDE it as d_out of csv_decode_volume, so
+ * the decode kernels store their rows straight into the receiver's volume (no
+ * NCCL data-path collective).  Replaces the gather of decompress_volume's
+ * thread pool result (container.py:470-478) across GPUs. */
+int csv_peer_alloc(int device, uint64_t bytes, void** d_ptr, uint8_t* handle64);
+int csv_peer_free(int device, void* d_ptr);
+int csv_peer_open(int device, const uint8_t* handle64, void** d_ptr);
+int csv_peer_close(int device, void* d_ptr);
+
 /* ---------------------------------------------------------------- frame bookkeeping
  * Device restatements of the steps around the batched cache decode. */
 

@@ -32,7 +32,7 @@ EXPORTS = (
     "csv_cache_mark_used", "csv_cache_assign", "csv_cache_state", "csv_cache_counters", "csv_cache_stack_heights",
     "csv_cache_read_state", "csv_cache_plan", "csv_cache_decode_fills", "csv_volume_stage_detail",
     "csv_cache_read_fills", "csv_detail_plan_greedy", "csv_rans_decode", "csv_rans_encode", "csv_build_pyramid",
-    "csv_downsample", "csv_decode_bricks_host",
+    "csv_downsample", "csv_decode_bricks_host", "csv_peer_alloc", "csv_peer_free", "csv_peer_open", "csv_peer_close",
 )
 
 
@@ -136,6 +136,14 @@ def lib():
         L.csv_rans_encode.argtypes = [P, P, P, U64, P, P, P, P, UP]
         L.csv_build_pyramid.restype = I
         L.csv_build_pyramid.argtypes = [P, U64, I, P, P, UP]
+        L.csv_peer_alloc.restype = I
+        L.csv_peer_alloc.argtypes = [I, U64, P, P]
+        L.csv_peer_free.restype = I
+        L.csv_peer_free.argtypes = [I, P]
+        L.csv_peer_open.restype = I
+        L.csv_peer_open.argtypes = [I, P, P]
+        L.csv_peer_close.restype = I
+        L.csv_peer_close.argtypes = [I, P]
         L.csv_decode_bricks_host.restype = I
         L.csv_decode_bricks_host.argtypes = [P, U64, P, P, P, P, UP]
         L.csv_downsample.restype = I

@@ -203,6 +203,18 @@ class GpuVolume:
                                                     _stream_handle(torch, stream)))
         return out, results
 
+    def decode_into(self, t: int, out_ptr: int, z_range, results, stream=None) -> None:
+        """Raster decode into raw device memory (z_range rows of the cropped volume at
+        out_ptr, row pitch cx): the peer-memory gather writes through pointers into
+        another rank's volume, which no local tensor describes."""
+        torch = self._torch
+        if not 0 <= t <= self.brick_log2:
+            raise ValueError(f"LOD {t} outside [0, {self.brick_log2}]")
+        _check_buffer("results", results, self.device, 8, min_numel=4 * self.n_bricks)
+        with _on_stream(torch, self.device, stream):
+            _lib.check(_lib.lib().csv_decode_volume(self._h, t, int(out_ptr), z_range[0], z_range[1], _ptr(results),
+                                                    _stream_handle(torch, stream)))
+
     def upload(self, blob: int, host: np.ndarray, offset: int, stream=None) -> None:
         """Fill bytes [offset, offset + host.nbytes) of blob 0 palette / 1 coarse / 2 detail (deferred volumes)."""
         torch = self._torch

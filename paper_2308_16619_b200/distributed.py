@@ -14,6 +14,13 @@ The only data exchange is the final gather of the decoded slabs:
   root's preallocated (Z, Y, X) volume -- each peer's slab lands in its own
   contiguous z-row view, the root decodes its own slab in place, no padding
   and no concatenation.
+* ``gather="peer"`` (fused decode + gather): the root allocates the volume as an
+  IPC-shareable buffer (csv_peer_alloc) and broadcasts its 64-byte handle; every
+  other rank maps it (csv_peer_open: NVLink peer memory on a multi-GPU node) and
+  decodes its slab with the output pointer INSIDE the root's volume, so the K2w
+  row stores go straight to the root while the rest of the slab is still being
+  decoded -- no NCCL data-path collective, no staging buffer.  The root returns a
+  PeerVolume (``.tensor()`` is the volume); the others return None.
 * ``gather="all"``: every rank ends with the volume.  Equal slabs (the
   2048^3 / 1024^3 workloads on 1, 2, 4, 8 ranks) use one
   ``all_gather_into_tensor`` into the output itself; unequal ones one
@@ -82,8 +89,10 @@ def agree_on_error(err, group=None):
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return err
-    allv = torch.empty((world, 4), dtype=torch.int64, device=err.device)
-    dist.all_gather_into_tensor(allv, err.reshape(1, 4).contiguous(), group=group)
+    # NCCL exchanges device tensors; gloo (CPU tests, the single-device peer test) host ones
+    dev = err.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    allv = torch.empty((world, 4), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allv, err.reshape(1, 4).to(dev).contiguous(), group=group)
     return allv[int(torch.argmin(allv[:, 0]))]
 
 
@@ -134,6 +143,119 @@ def gather_slabs(slab, out, dims, brick_log2: int, t: int, mode: str = "root", r
     return out
 
 
+class _CudaArray:
+    """A raw device pointer seen by torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(int(v) for v in shape), "typestr": "<i4",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class PeerVolume:
+    """The root's (cz, cy, cx) int32 volume in IPC-shareable device memory.
+
+    ``PeerVolume.alloc(shape, device)`` on the root (``handle`` = 64 bytes to publish),
+    ``PeerVolume.open(handle, shape, device)`` on the other ranks.  ``rows_ptr(z)`` is the
+    device address of row z (what a rank passes to the decode); ``tensor()`` views the
+    whole volume on the root.  ``close()`` frees (root) or unmaps (others)."""
+
+    def __init__(self, ptr: int, shape, device, handle: bytes, owner: bool):
+        self.ptr, self.shape, self.device, self.handle, self.owner = ptr, tuple(shape), device, handle, owner
+
+    @classmethod
+    def alloc(cls, shape, device):
+        import ctypes
+        from . import _lib
+        nbytes = 4 * int(np.prod(shape, dtype=np.int64))
+        p = ctypes.c_void_p()
+        h = (ctypes.c_uint8 * 64)()
+        _lib.check(_lib.lib().csv_peer_alloc(device.index, nbytes, ctypes.byref(p), h))
+        return cls(p.value, shape, device, bytes(h), True)
+
+    @classmethod
+    def open(cls, handle: bytes, shape, device):
+        import ctypes
+        from . import _lib
+        p = ctypes.c_void_p()
+        h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+        _lib.check(_lib.lib().csv_peer_open(device.index, h, ctypes.byref(p)))
+        return cls(p.value, shape, device, handle, False)
+
+    def rows_ptr(self, z: int) -> int:
+        return self.ptr + 4 * int(z) * self.shape[1] * self.shape[2]
+
+    def tensor(self):
+        import torch
+        t = torch.as_tensor(_CudaArray(self.ptr, self.shape), device=self.device)
+        t._peer_volume = self          # keep the allocation alive with the view
+        return t
+
+    def close(self) -> None:
+        from . import _lib
+        if self.ptr:
+            (_lib.lib().csv_peer_free if self.owner else _lib.lib().csv_peer_close)(self.device.index, self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def decompress_volume_peer(container, t: int = 0, group=None, root: int = 0):
+    """Fused decode + gather (``gather="peer"`` above): every rank decodes its
+    whole-bz-layer slab straight into the root's volume through peer memory.
+    Returns the root's PeerVolume on the root, None elsewhere; raises the
+    reference's exception for the globally lowest failing brick on every rank."""
+    import torch
+    import torch.distributed as dist
+    from . import _lib
+    torch_ = _lib.require_cuda()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    meta = container.meta
+    if not 0 <= t <= meta.brick_log2:
+        raise ValueError(f"LOD {t} outside [0, {meta.brick_log2}]")
+    x, y, z = meta.dims
+    shape = tuple(-(-d // (1 << t)) for d in (z, y, x))
+    dev = torch_.device("cuda", torch_.cuda.current_device())
+    pv = PeerVolume.alloc(shape, dev) if rank == root else None
+    if world > 1:
+        box = [pv.handle if pv is not None else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, root) if group is not None else root,
+                                   group=group)
+        if pv is None:
+            pv = PeerVolume.open(box[0], shape, dev)
+    b0, b1 = rank_bricks(meta.grid_dims, world, rank)
+    z0, z1 = rank_slab(meta.dims, meta.brick_log2, t, world, rank)
+    vol = container.to_device(device=dev, brick_range=(b0, b1))
+    try:
+        res = torch_.empty((max(vol.n_bricks, 1), 4), dtype=torch_.int64, device=dev)
+        if z1 > z0:
+            vol.decode_into(t, pv.rows_ptr(z0), (z0, z1), res)
+        torch_.cuda.current_stream(dev).synchronize()      # this rank's rows have landed in the root's volume
+        err = first_error(res, vol.n_bricks, b0, device=dev)
+        if t == meta.brick_log2 and vol.n_bricks and bool((res[:vol.n_bricks, 0] & 0xFFFFFFFF).eq(8).any()):
+            err = torch_.tensor([b0, -1, 0, 0], dtype=torch_.int64, device=dev)
+    finally:
+        vol.close()
+    err = agree_on_error(err, group)
+    if world > 1:
+        dist.barrier(group=group)                            # every slab is in place
+    if rank != root:
+        pv.close()
+    try:
+        if int(err[1]) == -1:
+            raise ValueError("expected 1 entries, got shape (0,)")
+        raise_agreed(err)
+    except Exception:
+        if rank == root:
+            pv.close()
+        raise
+    return pv if rank == root else None
+
+
 def decompress_volume_distributed(container, t: int = 0, group=None, gather: str | bool | None = "all",
                                   root: int = 0, out=None, decode_slab: Callable | None = None):
     """Decode this rank's whole-bz-layer slab and gather the cropped (Z, Y, X) volume.
@@ -153,6 +275,9 @@ def decompress_volume_distributed(container, t: int = 0, group=None, gather: str
     import torch.distributed as dist
     if gather is True:
         gather = "all"
+    if gather == "peer":
+        pv = decompress_volume_peer(container, t, group=group, root=root)
+        return pv.tensor() if pv is not None else None
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     meta = container.meta
