@@ -35,6 +35,9 @@
 #ifndef K1F_FMA_DECODE
 #define K1F_FMA_DECODE 1
 #endif
+#ifndef K1F_EVICT_FIRST
+#define K1F_EVICT_FIRST 1   // entry stores L2::evict_first (K1 DRAM reads 1.30x -> 1.18x of the stream bytes)
+#endif
 #ifndef K1F_BLOCK
 #define K1F_BLOCK 16
 #endif
@@ -55,6 +58,7 @@ struct FLane {
     uint32_t i, lim, n, len;
     uint32_t tb;            // shared-memory byte address of the stream's decode table
     uint64_t item;
+    uint64_t pol;           // L2 evict-first cache policy of the entry stores (K1F_EVICT_FIRST)
     bool pend;              // the top entry is a P_delta op waiting for its payload
     bool checked;           // exact per-step checks (corrupt stream or restart after an underrun)
 };
@@ -100,9 +104,17 @@ __device__ __forceinline__ void fl_flush(FLane& L) {
         uint32_t a0, a1, a2, a3, b0, b1, b2, b3;   // slots 0..3 = groups 3, 0, 1, 2 of the chunk
         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(L.ring) : "memory");
         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "r"(L.ring + 16u) : "memory");
+#if K1F_EVICT_FIRST
+        // entries stream through L2 (3.5 GB on config 3): evict them first so the lanes'
+        // stream bytes stay resident until consumed
+        asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;"
+                     :: "l"(reinterpret_cast<uint8_t*>(L.outp) + L.fl), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(b2),
+                        "r"(b3), "r"(a0), "r"(a1), "l"(L.pol) : "memory");
+#else
         asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
                      :: "l"(reinterpret_cast<uint8_t*>(L.outp) + L.fl), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(b2),
                         "r"(b3), "r"(a0), "r"(a1) : "memory");
+#endif
         L.fl += 32u;
     }
 }
@@ -291,6 +303,11 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_fast(VolView V, Plan P, u
     const uint64_t total = 2 * P.n;
     FLane L;
     L.ring = (uint32_t)__cvta_generic_to_shared(&ring[threadIdx.x][0]);
+#if K1F_EVICT_FIRST
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(L.pol));
+#else
+    L.pol = 0;
+#endif
     bool has = false, done = false;
     while (true) {
         const bool need = !has && !done;
