@@ -79,7 +79,7 @@ __device__ __forceinline__ uint32_t mode_first8(const uint32_t* v, bool* uniform
     return v[best];
 }
 
-struct EncLayout { uint32_t lev, cst, mask, wpre, words; };
+struct EncLayout { uint32_t lev, cst, mask, wpre, nmask, words; };
 __host__ __device__ inline EncLayout enc_layout(int N) {
     EncLayout Y;
     uint32_t nlev = 0;
@@ -90,7 +90,8 @@ __host__ __device__ inline EncLayout enc_layout(int N) {
     Y.cst = nlev;                                              // bytes: nlev, in words (nlev+3)/4
     Y.mask = Y.cst + (nlev + 3) / 4;
     Y.wpre = Y.mask + W;
-    Y.words = Y.wpre + W + 1;
+    Y.nmask = Y.wpre + W + 1;                                  // bytes: per parent, its palette-needing children
+    Y.words = Y.nmask + (maxP + 3) / 4;
     return Y;
 }
 
@@ -213,16 +214,15 @@ __global__ void __launch_bounds__(E_THREADS) e12_bricks(EncView E) {
         const uint32_t e0 = cursor[s];
         const int cbits = N - l + 1;
         const int64_t child_side = 1ll << cbits;
-        for (uint32_t base = 0; base < P; base += blockDim.x) {
-            const uint32_t m = base + threadIdx.x;
+        // pass 1: every active parent's 8 reuse ops (codec.py:150-181); the children that need a
+        // palette op are flagged per parent (nmask), their entries completed by the replay
+        uint8_t* const nmask = reinterpret_cast<uint8_t*>(ws + Y.nmask);
+        for (uint32_t m = threadIdx.x; m < P; m += blockDim.x) {
             uint32_t needmask = 0;
-            uint32_t labs[8];
-            uint64_t bytes = 0;
-            uint32_t rk = 0;
-            bool act = m < P && ((pmask[m >> 5] >> (m & 31)) & 1u);
-            if (act) {
-                rk = wpre[m >> 5] + __popc(pmask[m >> 5] & ((1u << (m & 31)) - 1u));
+            if ((pmask[m >> 5] >> (m & 31)) & 1u) {
+                const uint32_t rk = wpre[m >> 5] + __popc(pmask[m >> 5] & ((1u << (m & 31)) - 1u));
                 const uint32_t par = lp[m];
+                uint64_t bytes = 0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     const uint32_t j = (m << 3) | c;
@@ -247,35 +247,52 @@ __global__ void __launch_bounds__(E_THREADS) e12_bricks(EncView E) {
                         }
                     }
                     if (op == 7) needmask |= 1u << c;
-                    labs[c] = lab;
                     bytes |= (uint64_t)(op | (stop << 3)) << (8 * c);
                 }
                 *reinterpret_cast<uint64_t*>(es + e0 + 8 * rk) = bytes;
             }
-            // ordered compaction of palette-needing children (rank order == Morton order)
-            uint32_t k = __popc(needmask);
+            nmask[m] = (uint8_t)needmask;
+        }
+        __syncthreads();
+        // pass 2: ordered compaction (rank order == Morton order): each thread owns a contiguous
+        // run of parents, one block scan of the run totals, then the run's needs in order
+        {
+            const uint32_t per = (P + blockDim.x - 1) / blockDim.x;
+            const uint32_t m0 = min(P, threadIdx.x * per), m1 = min(P, m0 + per);
+            uint32_t cnt = 0;
+            for (uint32_t m = m0; m < m1; ++m) cnt += __popc((uint32_t)nmask[m]);
             const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-            uint32_t inc = k;
+            uint32_t inc = cnt;
             for (int o = 1; o < 32; o <<= 1) {
-                uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+                const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += u;
             }
             if (lane == 31) S.scan[wid] = inc;
             __syncthreads();
-            if (threadIdx.x == 0) {
-                uint32_t run = 0;
-                for (int w = 0; w < E_THREADS / 32; ++w) { uint32_t v = S.scan[w]; S.scan[w] = run; run += v; }
-                S.scan[E_THREADS / 32] = run;
+            if (threadIdx.x < 32) {
+                const uint32_t v = threadIdx.x < E_THREADS / 32 ? S.scan[threadIdx.x] : 0u;
+                uint32_t x = v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, x, o);
+                    if ((int)threadIdx.x >= o) x += u;
+                }
+                if (threadIdx.x < E_THREADS / 32) S.scan[threadIdx.x] = x - v;
+                if (threadIdx.x == E_THREADS / 32 - 1) S.scan[E_THREADS / 32] = x;
             }
             __syncthreads();
-            uint32_t pos = nneed + S.scan[wid] + inc - k;
-            if (needmask) {
-                for (int c = 0; c < 8; ++c) {
-                    if (!((needmask >> c) & 1u)) continue;
-                    uint32_t eidx = e0 + 8 * rk + c;
-                    uint32_t stop = (uint32_t)(bytes >> (8 * c + 3)) & 1u;
-                    need[2 * pos] = eidx | ((uint32_t)s << 31) | (stop << 30);
-                    need[2 * pos + 1] = labs[c];
+            uint32_t pos = nneed + S.scan[wid] + inc - cnt;
+            for (uint32_t m = m0; m < m1; ++m) {
+                uint32_t nmk = nmask[m];
+                if (!nmk) continue;
+                const uint32_t rk = wpre[m >> 5] + __popc(pmask[m >> 5] & ((1u << (m & 31)) - 1u));
+                while (nmk) {
+                    const int c = __ffs(nmk) - 1;
+                    nmk &= nmk - 1;
+                    const uint32_t j = (m << 3) | (uint32_t)c;
+                    const uint32_t lab = l > 1 ? lc[j] : voxel(E, ox + compact3(j), oy + compact3(j >> 1), oz + compact3(j >> 2));
+                    const uint32_t stop = (l > 1 && cc[j]) ? 1u : 0u;
+                    need[2 * pos] = (e0 + 8 * rk + (uint32_t)c) | ((uint32_t)s << 31) | (stop << 30);
+                    need[2 * pos + 1] = lab;
                     ++pos;
                 }
             }

@@ -5,7 +5,7 @@ import torch
 import paper_2308_16619_b200 as p
 vol = p.synth_voronoi((1024, 1024, 1024), 22, 3, False)
 ts = []
-for _ in range(4):
+for _ in range(int(os.environ.get("REPS", "4"))):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
