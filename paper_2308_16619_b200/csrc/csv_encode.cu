@@ -66,16 +66,19 @@ __device__ __forceinline__ uint32_t voxel(const EncView& E, int64_t x, int64_t y
 
 // mode of 8 with first-occurrence ties (pyramid.py:43-55); also "all equal"
 __device__ __forceinline__ uint32_t mode_first8(const uint32_t* v, bool* uniform) {
-    int best = 0, bestc = -1, c0 = 0;
+    int c0 = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int j = 0; j < 8; ++j) c0 += v[j] == v[0];
+    *uniform = c0 == 8;
+    if (c0 >= 4) return v[0];   // no other label can exceed it, and ties go to the first occurrence
+    int best = 0, bestc = c0;
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
         int cnt = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) cnt += v[j] == v[k];
-        if (k == 0) c0 = cnt;
         if (cnt > bestc) { bestc = cnt; best = k; }
     }
-    *uniform = c0 == 8;
     return v[best];
 }
 

@@ -29,16 +29,19 @@ constexpr uint32_t kPrec = 12;
 struct RansTable { uint32_t freq[16]; uint32_t cum[17]; };
 
 __device__ __forceinline__ uint32_t mode8(const uint32_t (&v)[8], bool* uniform) {
-    int best = 0, bestc = -1, c0 = 0;
+    int c0 = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int j = 0; j < 8; ++j) c0 += v[j] == v[0];
+    *uniform = c0 == 8;
+    if (c0 >= 4) return v[0];   // no other label can exceed it, and ties go to the first occurrence
+    int best = 0, bestc = c0;
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
         int cnt = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) cnt += v[j] == v[k];
-        if (k == 0) c0 = cnt;
         if (cnt > bestc) { bestc = cnt; best = k; }
     }
-    *uniform = c0 == 8;
     return v[best];
 }
 
