@@ -42,7 +42,8 @@ struct VolView {
     int fast_tab;              // every table count <= 4095: K1f's packed table applies
 };
 
-constexpr uint32_t kWScratch6Stride = 49152;   // K2w<6> scratch per warp slot (u16)
+constexpr uint32_t kWScratch6Stride = 57344;   // K2w<6> scratch per warp slot (u16): palette bases 32768,
+                                               // final parent level 16384 (32 KB), coarse list + descriptors 8192
 constexpr int kK2W6MaxWarpsPerSM = 8;          // K2w<6> warp slots per SM
 constexpr uint32_t kWScratchStride = 4096;   // K2w scratch per warp slot (final-level parents, LMAX <= 5)
 

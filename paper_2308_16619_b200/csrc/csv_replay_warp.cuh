@@ -84,8 +84,8 @@ __host__ __device__ constexpr WLayout make_wlayout(int L, uint32_t isz) {
         end = al16(end + 2 * R * R);
     }
     Y.clist = Y.ring;                                     // coarse levels: ring and plist are free
-    end = umax(end, al16(Y.ring + 4 * cpar));
-    Y.cdesc = Y.clist + 2 * cpar;
+    if (!gfin) end = umax(end, al16(Y.ring + 4 * cpar));  // (64^3 replays: the largest coarse level's
+    Y.cdesc = Y.clist + 2 * cpar;                         //  list lives in the warp's global slot)
     Y.spal = end;                                         // u8 mode: the brick's palette (<= 256 labels)
     if (isz == 1 && K2W_SPAL) end = al16(end + 1024);
     Y.amask = end;                                        // final level: per-plane active mask + word prefix (chain hops)
@@ -1094,9 +1094,11 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         B.Ed = P.entries + eo1;
         B.capd = (uint32_t)round32(limd);
         uint8_t* fin = nullptr;   // K2w<6>: the final parent level (32^3 u8) in the warp's global slot
+        uint16_t* glist = nullptr;   // K2w<6>: list + pending descriptors of the 16^3-parent coarse level
         if constexpr (LMAX >= 6) {
             B.ipb = P.wscratch6 + (uint64_t)(blockIdx.x * K2W_WARPS + (threadIdx.x >> 5)) * kWScratch6Stride;
             fin = reinterpret_cast<uint8_t*>(B.ipb + 32768);
+            glist = B.ipb + 32768 + 16384;
         } else {
             B.ipb = P.wscratch + (uint64_t)(blockIdx.x * K2W_WARPS + (threadIdx.x >> 5)) * P.wscratch_stride;
         }
@@ -1112,7 +1114,10 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         bool failed = false;
         for (int j = 0; j + 1 < B.n; ++j) {      // parents at level N - j, children above the final level
             IT* const finj = (LMAX >= 6 && j + 2 == B.n) ? reinterpret_cast<IT*>(fin) : nullptr;
-            const unsigned long long ek = coarse_level<IT>(B, j, lev, pm, cm, wpre, clist, cdesc, cur_c, ip_run, pdc,
+            // 64^3 replays: the 4096-parent level's list does not fit the warp's shared slice
+            uint16_t* const lj = (LMAX >= 6 && j == 4) ? glist : clist;
+            uint16_t* const dj = (LMAX >= 6 && j == 4) ? glist + 4096 : cdesc;
+            const unsigned long long ek = coarse_level<IT>(B, j, lev, pm, cm, wpre, lj, dj, cur_c, ip_run, pdc,
                                                            lane, finj);
             if (ek != ~0ull) { report_error(P, rr, B.Ec, B.capc, B.src, ek, false, lane); failed = true; break; }
             uint32_t* tmp = pm; pm = cm; cm = tmp;
