@@ -154,3 +154,30 @@ def test_random_corruption_matches_oracle(pkg, oracle, name):
             checked += 1
         vol.close()
     assert checked == 150 * len(reqs)
+
+
+def test_lod_decode_equals_independent_downsampler(pkg):
+    """SPEC.md:771 / pyramid.py:99-104: for dims that are multiples of the brick side,
+    the LOD-t decode of the whole volume equals the mode-of-8 downsampler applied t
+    times to the input (an oracle independent of the operation replay).  The
+    downsampler here is numpy, restated from pyramid.py:81-96 in the test itself."""
+    def down(g):
+        nz, ny, nx = g.shape
+        c = g.reshape(nz // 2, 2, ny // 2, 2, nx // 2, 2).transpose(0, 2, 4, 1, 3, 5).reshape(-1, 8)
+        cnt = (c[:, :, None] == c[:, None, :]).sum(axis=2)          # per slot: occurrences of its label
+        win = np.argmax(cnt, axis=1)                                # first slot with the maximal count
+        return c[np.arange(c.shape[0]), win].reshape(nz // 2, ny // 2, nx // 2)
+    rng = np.random.default_rng(17)
+    for case in range(6):
+        bl = int(rng.integers(2, 6))
+        side = 1 << bl
+        shape = tuple(int(side * v) for v in rng.integers(1, 4, size=3))
+        vol = _volume(rng, ["smooth", "membrane", "few", "noise"][case % 4], shape)
+        c = pkg.compress_volume(vol, pkg.CompressionConfig(brick_log2=bl))
+        ref = vol
+        for t in range(bl + 1):
+            if t:
+                ref = down(ref)
+            assert np.array_equal(pkg.decompress_volume(c, t), ref), (case, bl, shape, t)
+            if t <= 2:   # the GPU downsampler (csv_downsample) agrees with the numpy one
+                assert t == 0 or np.array_equal(pkg.downsample_volume(vol, t), ref), (case, t)
