@@ -17,7 +17,7 @@
 namespace csv {
 cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                        unsigned long long* counter, uint32_t* gws, uint64_t gws_stride, int gws_ctas,
-                       int nsm, int min_t, cudaStream_t st, cudaEvent_t* ev);
+                       int nsm, int min_t, cudaStream_t st, cudaEvent_t* ev, const Overlap* ov);
 cudaError_t run_root_raster(const VolView& V, Plan P, cudaStream_t st);
 cudaError_t run_streams_only(const VolView& V, Plan P, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                              unsigned long long* counter, int nsm, cudaStream_t st);
@@ -74,6 +74,7 @@ struct csv_volume {
     uint64_t blob_cap[3]{};         // bytes of the palette / coarse / detail slices held
     bool timing = false;
     cudaEvent_t ev[4]{};            // plan start, K1 start, K1 end / K2 start, K2 end
+    Overlap ovl{};                  // K1 -> K2w overlap side stream (run_decode)
     // csv_decode_bricks_host: pinned request staging + device requests / pool / results (grow-only)
     uint64_t hreq_cap = 0, hpool_cap = 0;
     uint8_t* h_req = nullptr;       // pinned: brick u32[cap] | lod u8[cap] (16-aligned) | dst u64[cap]
@@ -224,6 +225,9 @@ static void vol_release(csv_volume* v) {
     if (v->h_req) cudaFreeHost(v->h_req);
     cudaStreamSynchronize(0);
     for (auto& e : v->ev) if (e) cudaEventDestroy(e);
+    if (v->ovl.fork) cudaEventDestroy(v->ovl.fork);
+    if (v->ovl.join) cudaEventDestroy(v->ovl.join);
+    if (v->ovl.side) cudaStreamDestroy(v->ovl.side);
     delete v;
 }
 
@@ -243,7 +247,12 @@ static int ensure_plan(csv_volume* v, uint64_t n, uint64_t entries_need, int Lg,
         CUDA_TRY(dalloc(&v->d_wscratch6, (size_t)v->nsm * kK2W6MaxWarpsPerSM * kWScratch6Stride * sizeof(uint16_t), st));
     if (!v->d_scan) {
         CUDA_TRY(dalloc(&v->d_scan, 4104 * sizeof(uint64_t), st));
-        CUDA_TRY(dalloc(&v->d_counter, 4 * sizeof(unsigned long long), st));
+        CUDA_TRY(dalloc(&v->d_counter, kCounterSlots * sizeof(unsigned long long), st));
+    }
+    if (!v->ovl.side) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&v->ovl.side, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&v->ovl.fork, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&v->ovl.join, cudaEventDisableTiming));
     }
     if (entries_need + 64 > v->entries_cap) {
         if (v->d_entries) CUDA_TRY(cudaDeviceSynchronize());
@@ -514,7 +523,7 @@ int csv_decode_volume_range(csv_volume* vol, int t, uint64_t brick_first, uint64
     P.wscratch_stride = kWScratchStride;
     P.wscratch6 = vol->d_wscratch6;
     CUDA_TRY(run_decode(vol->V, P, 0, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
-                        vol->gws_ctas, vol->nsm, t, st, vol->timing ? vol->ev : nullptr));
+                        vol->gws_ctas, vol->nsm, t, st, vol->timing ? vol->ev : nullptr, &vol->ovl));
     return CSV_OK;
 }
 
@@ -548,7 +557,7 @@ int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, cons
     P.wscratch_stride = kWScratchStride;
     P.wscratch6 = vol->d_wscratch6;
     CUDA_TRY(run_decode(vol->V, P, 1, vol->d_sizes, vol->d_scan, vol->d_counter, vol->d_gws, vol->gws_stride,
-                        vol->gws_ctas, vol->nsm, 0, st, vol->timing ? vol->ev : nullptr));
+                        vol->gws_ctas, vol->nsm, 0, st, vol->timing ? vol->ev : nullptr, &vol->ovl));
     return CSV_OK;
 }
 

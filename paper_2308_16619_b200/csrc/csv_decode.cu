@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_plan_small(VolView V, Plan P, unsigned 
     }
     if (threadIdx.x == 0) {
         P.eoff[n2] = tot;
-        counter[0] = counter[1] = counter[2] = counter[3] = 0;
+        for (int i = 0; i < kCounterSlots; ++i) counter[i] = 0;
     }
 }
 
@@ -1029,31 +1029,53 @@ static void k2_launch_mode(int L, unsigned grid, size_t smem, const VolView& V, 
     }
 }
 // K2w: persistent warps (K2W_WARPS per CTA), as many CTAs as fit per SM
-template <int MODE, int L, typename IT>
-static void k2w_launch_one(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
+// per_sm > 0: the overlap launch (warps per SM beside K1), 0: as many warps as fit, < 0: only
+// the one-time set-up (function attributes, occupancy query -- which also loads the kernel).
+template <int MODE, int L, typename IT, bool Q = false>
+static void k2w_launch_one(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st,
+                           int per_sm = 0) {
     const size_t smem = (size_t)K2W_WARPS * wk::make_wlayout(L, sizeof(IT)).bytes;
     static int occ = 0;
     if (!occ) {
-        cudaFuncSetAttribute(k2_warp<MODE, L, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_warp<MODE, L, IT>, 32 * K2W_WARPS, smem);
+        cudaFuncSetAttribute(k2_warp<MODE, L, IT, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_warp<MODE, L, IT, Q>, 32 * K2W_WARPS, smem);
         if (occ < 1) occ = 1;
-        if (occ * K2W_WARPS > 64) occ = 64 / K2W_WARPS;   // wscratch holds 64 warp slots per SM
+        if (occ * K2W_WARPS > 32) occ = 32 / K2W_WARPS;   // wscratch: 64 warp slots per SM, the upper half for the overlap launch
         if (L >= 6 && occ * K2W_WARPS > kK2W6MaxWarpsPerSM) occ = kK2W6MaxWarpsPerSM / K2W_WARPS;   // wscratch6 slots
     }
+    if (per_sm < 0) return;   // prepare only: attributes set and the kernel loaded before K1 runs
     uint64_t want = (P.n + K2W_WARPS - 1) / K2W_WARPS;
-    uint64_t grid = (uint64_t)nsm * occ;
+    uint64_t grid = (uint64_t)nsm * (per_sm > 0 ? (uint64_t)per_sm / K2W_WARPS : (uint64_t)occ);
     if (grid > want) grid = want;
-    k2_warp<MODE, L, IT><<<(unsigned)grid, 32 * K2W_WARPS, smem, st>>>(V, P, counter);
+    if (grid < 1) grid = 1;
+    k2_warp<MODE, L, IT, Q><<<(unsigned)grid, 32 * K2W_WARPS, smem, st>>>(V, P, counter);
 }
-template <int MODE, typename IT>
-static void k2w_launch_mode(int L, const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
+template <int MODE, typename IT, bool Q = false>
+static void k2w_launch_mode(int L, const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st,
+                            int per_sm = 0) {
     switch (L) {
-        case 1: k2w_launch_one<MODE, 1, IT>(V, P, counter, nsm, st); break;
-        case 2: k2w_launch_one<MODE, 2, IT>(V, P, counter, nsm, st); break;
-        case 3: k2w_launch_one<MODE, 3, IT>(V, P, counter, nsm, st); break;
-        case 4: k2w_launch_one<MODE, 4, IT>(V, P, counter, nsm, st); break;
-        default: k2w_launch_one<MODE, 5, IT>(V, P, counter, nsm, st); break;
+        case 1: k2w_launch_one<MODE, 1, IT, Q>(V, P, counter, nsm, st, per_sm); break;
+        case 2: k2w_launch_one<MODE, 2, IT, Q>(V, P, counter, nsm, st, per_sm); break;
+        case 3: k2w_launch_one<MODE, 3, IT, Q>(V, P, counter, nsm, st, per_sm); break;
+        case 4: k2w_launch_one<MODE, 4, IT, Q>(V, P, counter, nsm, st, per_sm); break;
+        default: k2w_launch_one<MODE, 5, IT, Q>(V, P, counter, nsm, st, per_sm); break;
     }
+}
+// K1 -> K2w overlap: CSVGPU_OVERLAP=0 disables it; CSVGPU_OVL_WARPS overrides the overlap
+// launch's warps per SM.  Default: 16 when K1 has at most 2 blocks per SM (strong-scaling
+// shares of <= 8 bz layers), else 12 (measured on the config-3 shares and the config-4 batch;
+// more warps than fit beside K1 take the SMs K1's finished blocks leave).
+static int ovl_warps(uint64_t k1_blocks, int nsm) {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("CSVGPU_OVERLAP");
+        const char* w = getenv("CSVGPU_OVL_WARPS");
+        v = (e && strcmp(e, "0") == 0) ? 0 : (w ? atoi(w) : -1);
+        if (v < -1) v = 0;
+        if (v > 32) v = 32;
+    }
+    if (v >= 0) return v;
+    return k1_blocks <= 2ull * (uint64_t)nsm ? 16 : 12;
 }
 static bool k2w6_disabled() {
     static int v = -1;
@@ -1073,28 +1095,65 @@ static void launch_k2_smem(int mode, int L, unsigned grid, size_t smem, const Vo
 
 cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, uint64_t* scan_tmp,
                        unsigned long long* counter, uint32_t* gws, uint64_t gws_stride, int gws_ctas,
-                       int nsm, int min_t, cudaStream_t st, cudaEvent_t* ev) {
+                       int nsm, int min_t, cudaStream_t st, cudaEvent_t* ev, const Overlap* ov) {
     if (P.n == 0) return cudaSuccess;
+    // K2: shared-memory instantiation for N - t <= 5, global workspace above
+    int Ls = V.N - min_t;
+    if (Ls > 5) Ls = 5;
+    if (Ls < 1) Ls = 1;
+    const bool small = 2 * P.n <= (uint64_t)SCAN_ITEMS;
+    const bool k2w = V.max_pal <= 65535u && !k2w_disabled();
+    // K1 -> K2w overlap for plans K1 runs in one wave (strong-scaling shares, cache fills): K1's
+    // long chains leave the SMs idle at the end, so the u8 K2w pass starts on the bricks whose
+    // streams are done.  Needs K1f (it publishes the ready queue).  Not for multi-wave plans
+    // (the full volume): K1 then fills every SM to the end and the overlap costs 0.3 ms.
+    const uint64_t k1_blocks = (2 * P.n + K1_THREADS - 1) / K1_THREADS;
+    const int ow = ovl_warps(k1_blocks, nsm);
+    const bool ovl = ov && ov->side && ow > 0 && !small && k2w && V.entropy && V.fast_tab && !k1_old() &&
+                     k1_blocks > (uint64_t)kK1TinyBlocks && k1_blocks <= (uint64_t)nsm * K1_MINB_THROUGHPUT;
     if (ev) cudaEventRecord(ev[0], st);
-    if (2 * P.n <= (uint64_t)SCAN_ITEMS) {
+    if (small) {
         k_plan_small<<<1, 256, 0, st>>>(V, P, counter);
     } else {
         unsigned nb = (unsigned)((2 * P.n + 255) / 256);
         k_region_sizes<<<nb, 256, 0, st>>>(V, P, sizes_tmp);
         cudaError_t e = run_scan(sizes_tmp, P.eoff, 2 * P.n, scan_tmp, st);
         if (e != cudaSuccess) return e;
-        cudaMemsetAsync(counter, 0, 4 * sizeof(unsigned long long), st);   // K1 items, K2w u8 / u16 / 64^3 bricks
+        // K1 items, K2w u8 / u16 / 64^3 bricks, ready-queue tail
+        cudaMemsetAsync(counter, 0, kCounterSlots * sizeof(unsigned long long), st);
+        if (ovl) {   // the region sizes are dead after the scan: per-request counts + ready queue
+            P.rcnt = reinterpret_cast<uint32_t*>(sizes_tmp);
+            P.rq = P.rcnt + P.n;
+            P.rq_tail = counter + 4;
+            cudaMemsetAsync(sizes_tmp, 0, 2 * P.n * sizeof(uint32_t), st);
+        }
     }
     if (ev) cudaEventRecord(ev[1], st);
+    if (ovl) {
+        // The overlap launch spins on slots K1 publishes, so K1 must be launched FIRST and
+        // no host call may wait for the device in between: with lazy module loading, the
+        // first load of a kernel can wait for the running ones, which would wait for K1.
+        if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint8_t, true>(Ls, V, P, counter + 1, nsm, st, -1);
+        else k2w_launch_mode<OUT_MORTON, uint8_t, true>(Ls, V, P, counter + 1, nsm, st, -1);
+        cudaEventRecord(ov->fork, st);
+    }
     if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
     else launch_k1<false>(V, P, counter, nsm, st);
+    if (ovl) {   // overlap launch on the side stream, ordered after the plan, running beside K1
+        Plan Po = P;
+        Po.wslot0 = (uint32_t)nsm * 32u;
+        cudaStreamWaitEvent(ov->side, ov->fork, 0);
+        if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint8_t, true>(Ls, V, Po, counter + 1, nsm, ov->side, ow);
+        else k2w_launch_mode<OUT_MORTON, uint8_t, true>(Ls, V, Po, counter + 1, nsm, ov->side, ow);
+        cudaEventRecord(ov->join, ov->side);
+    }
     if (ev) cudaEventRecord(ev[2], st);
-    // K2: shared-memory instantiation for N - t <= 5, global workspace above
-    int Ls = V.N - min_t;
-    if (Ls > 5) Ls = 5;
-    if (Ls < 1) Ls = 1;
-    if (V.max_pal <= 65535u && !k2w_disabled()) {   // palette-index space: u8 pass, then u16 for long palettes
-        if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint8_t>(Ls, V, P, counter + 1, nsm, st);
+    if (k2w) {   // palette-index space: u8 pass, then u16 for long palettes
+        if (ovl) {   // the rest of the ready queue, at full occupancy once K1 is done
+            if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint8_t, true>(Ls, V, P, counter + 1, nsm, st);
+            else k2w_launch_mode<OUT_MORTON, uint8_t, true>(Ls, V, P, counter + 1, nsm, st);
+            cudaStreamWaitEvent(st, ov->join, 0);
+        } else if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint8_t>(Ls, V, P, counter + 1, nsm, st);
         else k2w_launch_mode<OUT_MORTON, uint8_t>(Ls, V, P, counter + 1, nsm, st);
         if (V.max_pal > e8::kMarkPal) {   // the u8 pass takes palettes of <= 253 labels (markers 253-255)
             if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint16_t>(Ls, V, P, counter + 2, nsm, st);

@@ -46,6 +46,13 @@ constexpr uint32_t kWScratch6Stride = 57344;   // K2w<6> scratch per warp slot (
                                                // final parent level 16384 (32 KB), coarse list + descriptors 8192
 constexpr int kK2W6MaxWarpsPerSM = 8;          // K2w<6> warp slots per SM
 constexpr uint32_t kWScratchStride = 4096;   // K2w scratch per warp slot (final-level parents, LMAX <= 5)
+constexpr int kCounterSlots = 8;              // work counters of one decode (K1 items, K2w passes, ready-queue tail)
+
+// Side stream + fork/join events of a volume's K1 -> K2w overlap launch (run_decode).
+struct Overlap {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
 
 // One decode call: n requests; request r decodes brick `brick[r]` at LOD lod[r].
 struct Plan {
@@ -68,6 +75,13 @@ struct Plan {
     uint16_t* wscratch6;       // K2w<6> (64^3 replays): per warp slot kWScratch6Stride u16 =
                                //   palette bases (32768 u16) + the final parent level (32768 u8)
     int k2w6;                  // K2w<6> serves the u8 bricks with N - t = 6 (k2_replay<6> skips them)
+    // K1 -> K2w overlap (single-wave plans): K1 counts finished streams per request in
+    // rcnt and appends a request to the ready queue rq (r + 1, 0 = not yet) once both of
+    // its streams are done; the u8 K2w pass takes queue slots instead of request indices.
+    uint32_t* rcnt;            // [n] or nullptr (no overlap)
+    uint32_t* rq;              // [n]
+    unsigned long long* rq_tail;
+    uint32_t wslot0;           // first wscratch warp slot of this K2w launch (the overlap launch runs beside another)
 };
 
 __device__ __forceinline__ uint64_t req_local(const VolView& V, const Plan& P, uint64_t r) {

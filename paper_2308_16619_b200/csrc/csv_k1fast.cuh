@@ -174,6 +174,21 @@ __device__ __forceinline__ void fl_step_fast(FLane& L) {
     fl_emit(L, e);
 }
 
+// K1 -> K2w overlap (Plan::rcnt): stream w of request w >> 1 is final (its entries and
+// csv_stream_result are written).  The second stream of a request to finish appends the
+// request to the ready queue with a release store; K2w's acquire load of the slot then
+// sees both streams' writes (each lane fences before its count increment).
+__device__ __forceinline__ void fl_signal(const Plan& P, uint64_t w) {
+    if (P.rcnt == nullptr) return;
+    __threadfence();
+    const uint64_t r = w >> 1;
+    if (atomicAdd(P.rcnt + r, 1u) == 1u) {
+        __threadfence();
+        const unsigned long long pos = atomicAdd(P.rq_tail, 1ull);
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(P.rq + pos), "r"((uint32_t)r + 1u) : "memory");
+    }
+}
+
 __device__ __forceinline__ void fl_finish(FLane& L, const Plan& P, bool failed) {
     const uint32_t ne = L.ne - (L.pend ? 1u : 0u);          // the pending P_delta op is not an entry
     for (; L.fl + 8u <= ne; L.fl += 8u) {                     // complete groups still in the ring
@@ -206,6 +221,7 @@ __device__ __forceinline__ void fl_finish(FLane& L, const Plan& P, bool failed) 
         r.partial_op = L.ahi >> 24;
     }
     P.sres[L.item] = r;
+    fl_signal(P, L.item);
 }
 
 // One symbol with the reference's checks; returns false when the lane's item is finished.
@@ -259,6 +275,7 @@ __device__ bool fl_init(FLane& L, const VolView& V, const Plan& P, uint64_t item
     L.tb = tab_s + ((uint32_t)s << 14);
     if (!ok) {
         P.sres[w] = csv_stream_result{0, 0xffffffffu, 0, 0};
+        fl_signal(P, w);
         return false;
     }
     const uint8_t* base = s ? V.detail + V.d_off[b] : V.coarse + V.c_off[b];
@@ -266,10 +283,12 @@ __device__ bool fl_init(FLane& L, const VolView& V, const Plan& P, uint64_t item
     if (L.lim == 0) {
         if (L.n == 0) P.sres[w] = csv_stream_result{0, 0, CSV_SF_FAILED | CSV_SF_COMPLETE, 0};
         else P.sres[w] = csv_stream_result{0, 0xffffffffu, 0, 0};
+        fl_signal(P, w);
         return false;
     }
     if (L.len < 4) {   // entropy stream shorter than its state word (codec.py:333-334)
         P.sres[w] = csv_stream_result{0, 0, CSV_SF_FAILED, 0};
+        fl_signal(P, w);
         return false;
     }
     L.x = (uint32_t)base[0] | ((uint32_t)base[1] << 8) | ((uint32_t)base[2] << 16) | ((uint32_t)base[3] << 24);

@@ -42,6 +42,15 @@ constexpr int kRUnroll = K2W_RUNROLL;
 
 namespace wk {
 
+// Entry words.  CG (the overlap launch, which reads regions while K1 is still running):
+// L2-coherent loads (ld.global.cg); otherwise the read-only path.  Each word is read once,
+// so L1 holds nothing useful either way; .cg costs ~1 % in the full-volume kernel.
+template <bool CG>
+__device__ __forceinline__ uint64_t ldent(const uint64_t* p) {
+    if constexpr (CG) return __ldcg(p);
+    else return __ldg(p);
+}
+
 __host__ __device__ constexpr uint32_t wofs(int j) {   // u16 offset of level N-j (root j = 0), 8-aligned
     return j == 0 ? 0u : 8u + ((1u << (3 * j)) - 8u) / 7u;
 }
@@ -346,6 +355,7 @@ __device__ __forceinline__ void store_children(const Brick& B, const Plan& P, ui
 }
 
 // Error epilogue (warp): status/stream/nibble position of the winning key.
+template <bool CG = false>
 __device__ __noinline__ void report_error(const Plan& P, uint64_t r, const uint8_t* Eb, uint32_t ecap,
                                           csv_stream_result sr, unsigned long long ek, bool leaf, int lane) {
     const uint32_t ent = (uint32_t)(ek >> 8);
@@ -363,7 +373,7 @@ __device__ __noinline__ void report_error(const Plan& P, uint64_t r, const uint8
     } else {
         uint32_t cnt = 0;      // nibble index of entry `ent` = ent + #payload nibbles before it
         for (uint32_t g = lane; g < (ent + 7) / 8; g += 32) {
-            uint64_t w = (8 * g + 8 <= ecap) ? __ldg(reinterpret_cast<const uint64_t*>(Eb) + g) : 0ull;
+            uint64_t w = (8 * g + 8 <= ecap) ? ldent<CG>(reinterpret_cast<const uint64_t*>(Eb) + g) : 0ull;
             uint32_t lim = ent - 8 * g;
             uint64_t m = m_op5(w);
             if (lim < 8) m &= (1ull << (8 * lim)) - 1ull;
@@ -389,7 +399,7 @@ __device__ __forceinline__ uint32_t morton_inc(uint32_t j, uint32_t M) { return 
 // ---------------------------------------------------------------- coarse level (Morton, smem)
 // Parents at level N - j (j bits per axis), children kept in the level array.
 // Returns the warp-uniform error key; adds the level's payload nibbles to pdl.
-template <typename IT>
+template <typename IT, bool CG = false>
 __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j, IT* lev, const uint32_t* pm,
                                                           uint32_t* cm, uint16_t* wpre, uint16_t* list,
                                                           uint16_t* pdesc, uint32_t& cur_c, uint32_t& ip_run,
@@ -421,7 +431,7 @@ __device__ __forceinline__ unsigned long long coarse_level(const Brick& B, int j
     for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
         const uint32_t k = k0 + lane;
         const uint32_t ent0 = e0 + 8 * k;
-        const uint64_t w = (k < nact && ent0 + 8 <= B.capc) ? __ldg(reinterpret_cast<const uint64_t*>(B.Ec + ent0)) : 0ull;
+        const uint64_t w = (k < nact && ent0 + 8 <= B.capc) ? ldent<CG>(reinterpret_cast<const uint64_t*>(B.Ec + ent0)) : 0ull;
         // palette base: i_p advances (P_a) of the preceding parents, in entry order (codec.py:453-457)
         const uint32_t c6 = __popcll(m_op6(w)), inc6 = warp_incl(c6, lane);
         const int32_t ipq = (int32_t)(ip_run + inc6 - c6);
@@ -533,7 +543,7 @@ __device__ __forceinline__ uint32_t child_off(uint32_t i, uint32_t c) {
 }
 
 // Ring voxel plane z (u16, (2R)^2) at ring + (z % 3) * (2R)^2; child (cx, cy) at cy * 2R + cx.
-template <int MODE, int RR, typename IT>
+template <int MODE, int RR, typename IT, bool CG = false>
 __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const Plan& P, const IT* plev,
                                                          const uint32_t* pm, uint16_t* wpre, IT* ring,
                                                          uint8_t* plist, uint16_t* pdesc, uint32_t* amask,
@@ -556,7 +566,7 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
     {
         auto ld = [&](uint32_t k) -> uint64_t {
             const uint32_t ent0 = e0 + 8 * k;
-            return (k < nact && ent0 + 8 <= cap) ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+            return (k < nact && ent0 + 8 <= cap) ? ldent<CG>(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
         };
         uint64_t wn = ld(lane), wnn = ld(32 + lane);   // two chunks in flight
         for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
@@ -622,7 +632,7 @@ __device__ __forceinline__ unsigned long long final_sweep(const Brick& B, const 
                 const uint32_t q = sx | sy | sz;
                 const uint32_t rank = wpre[q >> 5] + __popc(pm[q >> 5] & ((1u << (q & 31)) - 1u));
                 const uint32_t ent0 = e0 + 8 * rank;
-                const uint64_t w = ent0 + 8 <= cap ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+                const uint64_t w = ent0 + 8 <= cap ? ldent<CG>(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
                 const uint64_t vmask = valid_mask(nvalid, ent0);
                 const uint32_t pv = plev[q];
                 const uint32_t bf = (px == 0) | ((px == RR - 1) << 1) | ((py == 0) << 2) | ((py == RR - 1) << 3) |
@@ -841,7 +851,7 @@ __device__ __forceinline__ void resolve_rows(const Brick& B, uint8_t* pl, const 
 //     above, then x.
 // Resolution is fused with the whole-row raster write (each 16-byte row chunk
 // is resolved, written back for later readers and stored as labels).
-template <int MODE, int RR>
+template <int MODE, int RR, bool CG = false>
 __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const Plan& P, const uint8_t* plev,
                                                           const uint32_t* pm, uint16_t* wpre, uint8_t* ring,
                                                           uint8_t* plist_raw, uint32_t& cur, uint32_t& ip_run,
@@ -867,7 +877,7 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
     {   // palette base per active parent, in entry (rank) order (codec.py:453-457) -> per-warp scratch
         auto ld = [&](uint32_t k) -> uint64_t {
             const uint32_t ent0 = e0 + 8 * k;
-            return (k < nact && ent0 + 8 <= cap) ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+            return (k < nact && ent0 + 8 <= cap) ? ldent<CG>(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
         };
         uint64_t wn = ld(lane), wnn = ld(32 + lane);
         for (uint32_t k0 = 0; k0 < nact; k0 += 32) {
@@ -944,7 +954,7 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
                 const uint32_t q = spread3_u32(px) | (spread3_u32(py) << 1) | sz;
                 const uint32_t rank = wpre[q >> 5] + __popc(pm[q >> 5] & ((1u << (q & 31)) - 1u));
                 const uint32_t ent0 = e0 + 8 * rank;
-                const uint64_t w = ent0 + 8 <= cap ? __ldg(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
+                const uint64_t w = ent0 + 8 <= cap ? ldent<CG>(reinterpret_cast<const uint64_t*>(E + ent0)) : 0ull;
                 const uint64_t vmask = valid_mask(nvalid, ent0);
                 const uint32_t pv = plev[q];
                 const uint32_t bf = (px == 0) | ((px == RR - 1) << 1) | ((py == 0) << 2) | ((py == RR - 1) << 3) |
@@ -1007,7 +1017,21 @@ __device__ __forceinline__ unsigned long long final_sweep8(const Brick& B, const
 #endif
 constexpr int K2W_WARPS = K2W_WPB;
 
-template <int MODE, int LMAX, typename IT>
+// Overlap launch (Q): request k of the counter is the k-th entry of K1's ready queue.  The
+// slot is published by K1 (fl_signal) with a release store; the spin is bounded and traps
+// (a launch failure, never a hang) if the slot is never published.
+__device__ __noinline__ unsigned long long wait_ready(const Plan& P, unsigned long long k) {
+    uint32_t v;
+    for (uint32_t spin = 0;; ++spin) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(P.rq + k) : "memory");
+        if (v) break;
+        if (spin > (1u << 24)) __trap();
+        __nanosleep(256);
+    }
+    return v - 1u;
+}
+
+template <int MODE, int LMAX, typename IT, bool Q = false>
 __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, Plan P, unsigned long long* counter) {
     using namespace wk;
     constexpr WLayout Y = make_wlayout(LMAX, sizeof(IT));
@@ -1028,9 +1052,13 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
     while (true) {
         __syncwarp();
         unsigned long long rr = 0;
-        if (lane == 0) rr = atomicAdd(counter, 1ull);
+        if (lane == 0) {
+            rr = atomicAdd(counter, 1ull);
+            if (Q && rr < P.n) rr = wait_ready(P, rr);
+        }
         rr = __shfl_sync(FULL, rr, 0);
         if (rr >= P.n) break;
+        if (Q) __syncwarp();   // lane 0's acquire orders the whole warp's reads of the brick's entries
         Brick B{};
         B.r = rr;
         const uint64_t b = req_local(V, P, rr);
@@ -1081,8 +1109,12 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
             if (nc_raw > 0 && V.c_bytes[b] < 4) { if (lane == 0) put_result(P, rr, CSV_ST_UNDERRUN, 0, 0, 0, 0); continue; }
             if (B.t == 0 && nd_raw > 0 && V.d_bytes[b] < 4) { if (lane == 0) put_result(P, rr, CSV_ST_UNDERRUN, 1, 0, 0, 0); continue; }
         }
-        B.src = P.sres[2 * rr];
-        B.srd = P.sres[2 * rr + 1];
+        {   // stream results through L2 (written by K1, possibly during this launch)
+            const uint4 a = __ldcg(reinterpret_cast<const uint4*>(P.sres + 2 * rr));
+            const uint4 c = __ldcg(reinterpret_cast<const uint4*>(P.sres + 2 * rr + 1));
+            memcpy(&B.src, &a, sizeof a);
+            memcpy(&B.srd, &c, sizeof c);
+        }
         const uint64_t eo0 = P.eoff[2 * rr], eo1 = P.eoff[2 * rr + 1], eo2 = P.eoff[2 * rr + 2];
         if (lane == 0 && eo2 > eo0) {   // stage this brick's entries + gip in L2 ahead of the levels
             const uint64_t lo = eo0 & ~15ull, hi = (eo2 + 15) & ~15ull;
@@ -1100,7 +1132,7 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
             fin = reinterpret_cast<uint8_t*>(B.ipb + 32768);
             glist = B.ipb + 32768 + 16384;
         } else {
-            B.ipb = P.wscratch + (uint64_t)(blockIdx.x * K2W_WARPS + (threadIdx.x >> 5)) * P.wscratch_stride;
+            B.ipb = P.wscratch + (uint64_t)(P.wslot0 + blockIdx.x * K2W_WARPS + (threadIdx.x >> 5)) * P.wscratch_stride;
         }
         const bool trivial = (uint64_t)nc + nd == 0;     // relevant == 0: fill palette[0] (codec.py:353-358)
         if (lane == 0) {
@@ -1117,9 +1149,9 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
             // 64^3 replays: the 4096-parent level's list does not fit the warp's shared slice
             uint16_t* const lj = (LMAX >= 6 && j == 4) ? glist : clist;
             uint16_t* const dj = (LMAX >= 6 && j == 4) ? glist + 4096 : cdesc;
-            const unsigned long long ek = coarse_level<IT>(B, j, lev, pm, cm, wpre, lj, dj, cur_c, ip_run, pdc,
+            const unsigned long long ek = coarse_level<IT, Q>(B, j, lev, pm, cm, wpre, lj, dj, cur_c, ip_run, pdc,
                                                            lane, finj);
-            if (ek != ~0ull) { report_error(P, rr, B.Ec, B.capc, B.src, ek, false, lane); failed = true; break; }
+            if (ek != ~0ull) { report_error<Q>(P, rr, B.Ec, B.capc, B.src, ek, false, lane); failed = true; break; }
             uint32_t* tmp = pm; pm = cm; cm = tmp;
         }
         if (failed) continue;
@@ -1131,25 +1163,25 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
         unsigned long long ek;
         if constexpr (sizeof(IT) == 1) {
             switch (B.n) {
-                case 1: ek = final_sweep<MODE, 1, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
-                case 2: ek = final_sweep<MODE, 2, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
-                case 3: ek = final_sweep8<MODE, 4>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
-                case 4: ek = final_sweep8<MODE, (LMAX >= 4 ? 8 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
-                case 5: ek = final_sweep8<MODE, (LMAX >= 5 ? 16 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
-                default: ek = final_sweep8<MODE, (LMAX >= 6 ? 32 : 4)>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+                case 1: ek = final_sweep<MODE, 1, IT, Q>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 2: ek = final_sweep<MODE, 2, IT, Q>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 3: ek = final_sweep8<MODE, 4, Q>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+                case 4: ek = final_sweep8<MODE, (LMAX >= 4 ? 8 : 4), Q>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+                case 5: ek = final_sweep8<MODE, (LMAX >= 5 ? 16 : 4), Q>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
+                default: ek = final_sweep8<MODE, (LMAX >= 6 ? 32 : 4), Q>(B, P, plev, pm, wpre, ring, plist, cur, ip_run, pdl, lane); break;
             }
         } else {
             switch (B.n) {
-                case 1: ek = final_sweep<MODE, 1, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
-                case 2: ek = final_sweep<MODE, 2, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
-                case 3: ek = final_sweep<MODE, 4, IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
-                case 4: ek = final_sweep<MODE, (LMAX >= 4 ? 8 : 1), IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
-                default: ek = final_sweep<MODE, (LMAX >= 5 ? 16 : 1), IT>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 1: ek = final_sweep<MODE, 1, IT, Q>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 2: ek = final_sweep<MODE, 2, IT, Q>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 3: ek = final_sweep<MODE, 4, IT, Q>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                case 4: ek = final_sweep<MODE, (LMAX >= 4 ? 8 : 1), IT, Q>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
+                default: ek = final_sweep<MODE, (LMAX >= 5 ? 16 : 1), IT, Q>(B, P, plev, pm, wpre, ring, plist, fdesc, amask, cur, ip_run, pdl, lane); break;
             }
         }
         if (ek != ~0ull) {
-            if (B.t == 0) report_error(P, rr, B.Ed, B.capd, B.srd, ek, true, lane);
-            else report_error(P, rr, B.Ec, B.capc, B.src, ek, false, lane);
+            if (B.t == 0) report_error<Q>(P, rr, B.Ed, B.capd, B.srd, ek, true, lane);
+            else report_error<Q>(P, rr, B.Ec, B.capc, B.src, ek, false, lane);
             continue;
         }
         const int64_t ci = (int64_t)cur_c + warp_sum(pdc), di = (int64_t)cur_d + warp_sum(pdd);

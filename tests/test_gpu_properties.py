@@ -156,6 +156,56 @@ def test_random_corruption_matches_oracle(pkg, oracle, name):
     assert checked == 150 * len(reqs)
 
 
+@pytest.mark.parametrize("name", ["d_b5_mem", "a_b3"])
+def test_overlap_plan_with_corruption_matches_oracle(pkg, oracle, name):
+    """Batches of > 2048 requests take the K1 -> K2w overlap (K1 publishes finished
+    bricks to a ready queue, the u8 K2w pass starts on them while K1 still runs): every
+    brick at LOD 0-2, repeated until the plan is large enough, under random stream
+    corruption, vs the oracle's per-brick decode (status, stream, nibble / labels and
+    consumed counts)."""
+    import torch
+    import zlib
+    from conftest import golden_bytes
+    base = bytearray(golden_bytes(name))
+    c0 = pkg.CsvContainer.from_bytes(bytes(base))
+    N = c0.meta.brick_log2
+    n = c0.meta.brick_count
+    start = 120 + 44 * n
+    rng = np.random.default_rng(zlib.crc32(b"ovl" + name.encode()))
+    ts = [t for t in (0, 1, 2) if t < N]
+    one = [(i, t) for i in range(n) for t in ts]
+    reqs = one * (4200 // len(one) + 1)
+    assert len(reqs) > 4096
+    order = rng.permutation(len(reqs))
+    reqs = [reqs[k] for k in order]
+    sizes = np.array([8 ** (N - t) for _, t in reqs], dtype=np.int64)
+    dst = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    bricks = torch.tensor([r[0] for r in reqs], dtype=torch.int32, device="cuda")
+    lods = torch.tensor([r[1] for r in reqs], dtype=torch.uint8, device="cuda")
+    d_dst = torch.from_numpy(dst).cuda()
+    pool = torch.zeros(int(sizes.sum()), dtype=torch.int32, device="cuda")
+    for case in range(12):
+        data = bytearray(base)
+        for _ in range(int(rng.integers(0, 4)) if case else 0):
+            data[int(rng.integers(start, len(data)))] ^= int(rng.integers(1, 256))
+        c = pkg.CsvContainer.from_bytes(bytes(data))
+        oc = oracle.Container.from_bytes(bytes(data))
+        vol = c.to_device()
+        res = pkg.GpuVolume.results_host(vol.decode_bricks(bricks, lods, d_dst, pool), len(reqs))
+        host = pool.cpu().numpy().view(np.uint32)
+        ref = {key: oracle.container_decode_brick(oc, *key) for key in one}
+        for k, key in enumerate(reqs):
+            r_ref, out_ref = ref[key]
+            if r_ref[0] != 0:
+                assert (int(res[k]["status"]), int(res[k]["stream"]), int(res[k]["pos"])) == tuple(r_ref[:3]), \
+                    (name, case, key)
+            else:
+                assert int(res[k]["status"]) == 0, (name, case, key, res[k])
+                assert (int(res[k]["ci"]), int(res[k]["di"])) == (r_ref[3], r_ref[4]), (name, case, key)
+                assert np.array_equal(host[dst[k]: dst[k] + sizes[k]], out_ref), (name, case, key)
+        vol.close()
+
+
 def test_lod_decode_equals_independent_downsampler(pkg):
     """SPEC.md:771 / pyramid.py:99-104: for dims that are multiples of the brick side,
     the LOD-t decode of the whole volume equals the mode-of-8 downsampler applied t
