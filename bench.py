@@ -374,11 +374,23 @@ def timeseries_leg(p, torch, dev, stream, world: int = 1, rank: int = 0, total: 
     by <= k voxels at step k) sharded over the ranks (rank r takes timesteps r, r + N, ...;
     2 per rank at N = 8, 16 on one GPU); per timestep GPU encode then GPU decode, both
     timed with CUDA events (the decode after one untimed call that allocates the new
-    volume's workspace); lossless round trip checked (untimed).  Ensemble throughput =
+    volume's workspace; one untimed encode + decode before the first timestep); lossless
+    round trip checked (untimed).  Ensemble throughput =
     16 * 1024^3 voxels / the slowest rank's summed encode (decode) time."""
     enc_ms, dec_ms = [], []
     X, Y, Z = dims
     mine = list(range(rank, total, world))
+    # warm-up (untimed): one encode + decode, so that kernel loading and the encoder's
+    # one-time scratch arena / memory-pool growth are not charged to the first timestep
+    vol = p.synth_voronoi(dims, cells, seed=3, membrane=False, drift=0.0, drift_seed=3, device=dev)
+    enc = p.compress_volume_device(vol, p.CompressionConfig(brick_log2=BRICK_LOG2))
+    gv = enc.to_volume()
+    out = torch.empty_like(vol)
+    gv.decode(0, out=out)
+    torch.cuda.synchronize()
+    gv.close()
+    enc.close()
+    del vol, out
     for k in mine:
         vol = p.synth_voronoi(dims, cells, seed=3, membrane=False, drift=float(min(k, 16)), drift_seed=3 + k,
                               device=dev)

@@ -597,6 +597,8 @@ struct Scratch {
 struct ScratchArena {
     std::mutex mu;
     Scratch s;
+    uint64_t budget = 0;        // chunk scratch budget, fixed at the first encode on the device
+    bool pool_ready = false;    // default memory pool kept (release threshold) for the output blobs
 };
 constexpr int kMaxDevices = 64;
 ScratchArena g_arena[kMaxDevices];
@@ -614,19 +616,29 @@ cudaError_t reserve(T** p, uint64_t* cap, uint64_t bytes) {
 
 }  // namespace
 
+// Output blobs and the directory come from the device's default memory pool (stream-ordered,
+// kept by a release threshold): per-timestep encodes reuse the same physical pages instead of
+// paying cudaMalloc/cudaFree page mapping (which made a 1024^3 encode take 14-120 ms).
 static cudaError_t grow(void** p, uint64_t* cap, uint64_t need, uint64_t used, cudaStream_t st) {
     if (need <= *cap) return cudaSuccess;
     uint64_t nc = std::max<uint64_t>(need + 64, *cap * 3 / 2 + 64);
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, nc);
+    cudaError_t e = cudaMallocAsync(&q, nc, st);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(q, 0, nc, st);
     if (*p && used) cudaMemcpyAsync(q, *p, used, cudaMemcpyDeviceToDevice, st);
-    cudaStreamSynchronize(st);
-    cudaFree(*p);
+    if (*p) cudaFreeAsync(*p, st);
     *p = q;
     *cap = nc;
     return cudaSuccess;
+}
+
+static void keep_default_pool(int device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
 }
 
 extern "C" {
@@ -677,19 +689,27 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
         std::fprintf(stderr, "[enc] %8.2f ms  %s %lld\n", ms, what, k);
     };
-    size_t freeb = 0, totb = 0;
-    cudaMemGetInfo(&freeb, &totb);
-    mark("meminfo", 0);
-    // chunk scratch budget (grow-only arena): CSVGPU_ENC_BUDGET_GB overrides the default
-    // (8 GB: a 1024^3 volume of 32^3 bricks encodes in 2 chunks, 16.4 ms; 2 GB: 8 chunks, 25.5 ms)
-    static const double budget_gb = std::getenv("CSVGPU_ENC_BUDGET_GB") ? std::atof(std::getenv("CSVGPU_ENC_BUDGET_GB")) : 8.0;
-    uint64_t budget = std::min<uint64_t>((uint64_t)(freeb * 0.35), (uint64_t)(budget_gb * (1ull << 30)));
-    uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, budget / per_brick));
-    chunk = std::min<uint64_t>(chunk, 65536);
-
     if (device < 0 || device >= kMaxDevices) return efail(CSV_E_ARG, "device index out of range");
     std::lock_guard<std::mutex> arena_lock(g_arena[device].mu);
     Scratch& Sc = g_arena[device].s;
+    if (!g_arena[device].budget) {
+        // chunk scratch budget, sized once per device (cudaMemGetInfo waits for the driver's
+        // deferred frees: 15-90 ms inside a timed encode).  CSVGPU_ENC_BUDGET_GB overrides the
+        // default (8 GB: a 1024^3 volume of 32^3 bricks encodes in 2 chunks; 2 GB: 8 chunks, +55 %)
+        size_t freeb = 0, totb = 0;
+        cudaMemGetInfo(&freeb, &totb);
+        const char* bg = std::getenv("CSVGPU_ENC_BUDGET_GB");
+        const double budget_gb = bg ? std::atof(bg) : 8.0;
+        g_arena[device].budget = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)(freeb * 0.35),
+                                                                           (uint64_t)(budget_gb * (1ull << 30))));
+    }
+    if (!g_arena[device].pool_ready) {
+        keep_default_pool(device);
+        g_arena[device].pool_ready = true;
+    }
+    mark("budget", 0);
+    uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(n, g_arena[device].budget / per_brick));
+    chunk = std::min<uint64_t>(chunk, 65536);
     csv_encoded* enc = new csv_encoded();
     enc->device = device;
     enc->n = n;
@@ -711,7 +731,7 @@ int csv_encode_volume(int device, const void* d_volume, int width, int64_t X, in
     ETRY(reserve(&Sc.offs, &Sc.cap[6], (3 * chunk + 1) * 8));
     ETRY(reserve(&Sc.tmp, &Sc.cap[7], 4104 * 8));
     ETRY(reserve(&Sc.hist, &Sc.cap[8], 32 * 8));
-    ETRY(cudaMalloc(&enc->d_dir, n * 44 + 16));
+    ETRY(cudaMallocAsync(reinterpret_cast<void**>(&enc->d_dir), n * 44 + 16, st));
     if (smem) ETRY(cudaFuncSetAttribute(e12_bricks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
     mark("scratch reserved, chunk", (long long)chunk);
 
