@@ -197,10 +197,10 @@ class CsvContainer:
         res = np.zeros(1, dtype=_lib.RESULT_DTYPE)
         req_b = np.array([index], dtype=np.uint32)
         req_l = np.array([t], dtype=np.uint8)
-        with torch.cuda.device(vol.device):
-            _lib.check(_lib.lib().csv_decode_bricks_host(vol._h, 1, req_b.ctypes.data, req_l.ctypes.data,
-                                                          out.ctypes.data, res.ctypes.data,
-                                                          torch.cuda.current_stream(vol.device).cuda_stream))
+        # the C-ABI selects the volume's device itself (cudaSetDevice); the stream is the caller's current one
+        _lib.check(_lib.lib().csv_decode_bricks_host(vol._h, 1, req_b.ctypes.data, req_l.ctypes.data,
+                                                      out.ctypes.data, res.ctypes.data,
+                                                      torch.cuda.current_stream(vol.device).cuda_stream))
         if res["status"][0] != 0:
             raise status_error(int(res["status"][0]), int(res["stream"][0]), int(res["pos"][0]))
         return out

@@ -81,7 +81,21 @@ struct csv_volume {
     uint8_t* d_req = nullptr;       // same layout on the device
     csv_result* d_hres = nullptr;
     uint32_t* d_hpool = nullptr;
+    // per-brick calls (n <= kBrickGraphMax): the request copy, the decode launches and the two
+    // copy-backs (into pinned staging) replayed as ONE CUDA graph, keyed by (n, voxels) and the
+    // workspace pointers; captured on the second call with a key (the first one sizes the
+    // workspace and loads the kernels), on a private stream
+    struct BrickGraph {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t n = 0, total = 0, seen = 0;
+        const void* ptrs[8]{};
+    } bgraph[8];
+    uint32_t bg_next = 0;
+    cudaStream_t cap_stream = nullptr;
+    uint8_t* h_bout = nullptr;      // pinned: labels then results of a graph replay
+    uint64_t h_bout_cap = 0;
 };
+constexpr uint64_t kBrickGraphMax = 16;
 
 // ---------------------------------------------------------------------------- kernels local to the API
 // Unpack 44-byte directory rows (container.py:53-64) into SoA, rebasing global
@@ -223,6 +237,9 @@ static void vol_release(csv_volume* v) {
     dfree(v->d_counter); dfree(v->d_entries); dfree(v->d_gws); dfree(v->d_wscratch); dfree(v->d_wscratch6);
     dfree(v->d_req); dfree(v->d_hres); dfree(v->d_hpool);
     if (v->h_req) cudaFreeHost(v->h_req);
+    for (auto& g : v->bgraph) if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (v->cap_stream) cudaStreamDestroy(v->cap_stream);
+    if (v->h_bout) cudaFreeHost(v->h_bout);
     cudaStreamSynchronize(0);
     for (auto& e : v->ev) if (e) cudaEventDestroy(e);
     if (v->ovl.fork) cudaEventDestroy(v->ovl.fork);
@@ -246,7 +263,7 @@ static int ensure_plan(csv_volume* v, uint64_t n, uint64_t entries_need, int Lg,
     if (!v->d_wscratch6 && v->V.N >= 6)
         CUDA_TRY(dalloc(&v->d_wscratch6, (size_t)v->nsm * kK2W6MaxWarpsPerSM * kWScratch6Stride * sizeof(uint16_t), st));
     if (!v->d_scan) {
-        CUDA_TRY(dalloc(&v->d_scan, 4104 * sizeof(uint64_t), st));
+        CUDA_TRY(dalloc(&v->d_scan, (kScanTmpSlots + 512) * sizeof(uint64_t), st));
         CUDA_TRY(dalloc(&v->d_counter, kCounterSlots * sizeof(unsigned long long), st));
     }
     if (!v->ovl.side) {
@@ -564,6 +581,12 @@ int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, cons
 // Per-brick host API: requests and labels in host memory, one call per batch
 // (CsvContainer.decode_brick's device-resident path).  Requests go through a
 // pinned staging buffer in one copy; outputs land contiguously in request order.
+static bool brick_graph_enabled() {   // CSVGPU_BRICK_GRAPH=0: per-brick calls launch directly
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("CSVGPU_BRICK_GRAPH"); v = (e && strcmp(e, "0") == 0) ? 0 : 1; }
+    return v == 1;
+}
+
 int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick, const uint8_t* h_lod,
                            uint32_t* h_out, csv_result* h_res, uintptr_t stream) {
     if (!vol || (n && (!h_brick || !h_lod || !h_out || !h_res))) return fail(CSV_E_ARG, "null argument");
@@ -602,6 +625,80 @@ int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick,
     }
     memcpy(h, h_brick, 4 * n);
     memcpy(h + lod_off, h_lod, n);
+    if (n <= kBrickGraphMax && !vol->timing && brick_graph_enabled()) {
+        // graph replay: same launches and copies as below, labels and results through pinned staging
+        const uint64_t out_bytes = total * sizeof(uint32_t), res_off = (out_bytes + 15) & ~15ull;
+        const uint64_t stage = res_off + n * sizeof(csv_result);
+        if (stage > vol->h_bout_cap) {
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if (vol->h_bout) cudaFreeHost(vol->h_bout);
+            vol->h_bout = nullptr;
+            vol->h_bout_cap = 0;
+            CUDA_TRY(cudaMallocHost(&vol->h_bout, std::max<uint64_t>(stage, 4096)));
+            vol->h_bout_cap = std::max<uint64_t>(stage, 4096);
+        }
+        const void* ptrs[8] = {vol->h_req, vol->d_req, vol->d_hpool, vol->d_hres, vol->h_bout, vol->d_eoff,
+                               vol->d_entries, vol->d_sizes};
+        csv_volume::BrickGraph* g = nullptr;
+        for (auto& c : vol->bgraph)
+            if (c.seen && c.n == n && c.total == total && memcmp(c.ptrs, ptrs, sizeof(ptrs)) == 0) g = &c;
+        if (g && g->exec) {
+            CUDA_TRY(cudaGraphLaunch(g->exec, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            memcpy(h_out, vol->h_bout, out_bytes);
+            memcpy(h_res, vol->h_bout + res_off, n * sizeof(csv_result));
+            return CSV_OK;
+        }
+        if (g) {   // second call with this key: capture
+            if (!vol->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&vol->cap_stream, cudaStreamNonBlocking));
+            cudaStream_t cs = vol->cap_stream;
+            cudaGraph_t graph = nullptr;
+            CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            cudaMemcpyAsync(vol->d_req, h, req_bytes, cudaMemcpyHostToDevice, cs);
+            const int rc = csv_decode_bricks(vol, n, reinterpret_cast<const uint32_t*>(vol->d_req), vol->d_req + lod_off,
+                                             reinterpret_cast<const uint64_t*>(vol->d_req + dst_off), vol->d_hpool,
+                                             vol->d_hres, reinterpret_cast<uintptr_t>(cs));
+            cudaMemcpyAsync(vol->h_bout, vol->d_hpool, out_bytes, cudaMemcpyDeviceToHost, cs);
+            cudaMemcpyAsync(vol->h_bout + res_off, vol->d_hres, n * sizeof(csv_result), cudaMemcpyDeviceToHost, cs);
+            const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+            if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+            CUDA_TRY(ce);
+            const void* now[8] = {vol->h_req, vol->d_req, vol->d_hpool, vol->d_hres, vol->h_bout, vol->d_eoff,
+                                  vol->d_entries, vol->d_sizes};
+            if (memcmp(now, ptrs, sizeof(ptrs)) != 0) {   // the decode grew a workspace during capture: not replayable
+                cudaGraphDestroy(graph);
+                g->seen = 0;
+                return fail(CSV_E_CUDA, "per-brick graph capture reallocated a workspace");
+            }
+            const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+            cudaGraphDestroy(graph);
+            CUDA_TRY(ie);
+            CUDA_TRY(cudaGraphLaunch(g->exec, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            memcpy(h_out, vol->h_bout, out_bytes);
+            memcpy(h_res, vol->h_bout + res_off, n * sizeof(csv_result));
+            return CSV_OK;
+        }
+        // first call with this key: run directly (sizes the workspace), remember the key
+        CUDA_TRY(cudaMemcpyAsync(vol->d_req, h, req_bytes, cudaMemcpyHostToDevice, st));
+        const int rc = csv_decode_bricks(vol, n, reinterpret_cast<const uint32_t*>(vol->d_req), vol->d_req + lod_off,
+                                         reinterpret_cast<const uint64_t*>(vol->d_req + dst_off), vol->d_hpool,
+                                         vol->d_hres, stream);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(h_res, vol->d_hres, n * sizeof(csv_result), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(h_out, vol->d_hpool, out_bytes, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        const void* now[8] = {vol->h_req, vol->d_req, vol->d_hpool, vol->d_hres, vol->h_bout, vol->d_eoff,
+                              vol->d_entries, vol->d_sizes};
+        csv_volume::BrickGraph& c = vol->bgraph[vol->bg_next++ % 8];
+        if (c.exec) cudaGraphExecDestroy(c.exec);
+        c.exec = nullptr;
+        c.n = n;
+        c.total = total;
+        c.seen = 1;
+        memcpy(c.ptrs, now, sizeof(now));
+        return CSV_OK;
+    }
     CUDA_TRY(cudaMemcpyAsync(vol->d_req, h, req_bytes, cudaMemcpyHostToDevice, st));
     const int rc = csv_decode_bricks(vol, n, reinterpret_cast<const uint32_t*>(vol->d_req), vol->d_req + lod_off,
                                      reinterpret_cast<const uint64_t*>(vol->d_req + dst_off), vol->d_hpool, vol->d_hres,

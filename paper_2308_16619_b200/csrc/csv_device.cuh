@@ -46,6 +46,7 @@ constexpr uint32_t kWScratch6Stride = 57344;   // K2w<6> scratch per warp slot (
                                                // final parent level 16384 (32 KB), coarse list + descriptors 8192
 constexpr int kK2W6MaxWarpsPerSM = 8;          // K2w<6> warp slots per SM
 constexpr uint32_t kWScratchStride = 4096;   // K2w scratch per warp slot (final-level parents, LMAX <= 5)
+constexpr int kScanTmpSlots = 4104;           // u64 scan workspace (4096 block sums + total + pad)
 constexpr int kCounterSlots = 8;              // work counters of one decode (K1 items, K2w passes, ready-queue tail)
 
 // Side stream + fork/join events of a volume's K1 -> K2w overlap launch (run_decode).
