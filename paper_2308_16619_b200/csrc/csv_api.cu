@@ -81,18 +81,21 @@ struct csv_volume {
     uint8_t* d_req = nullptr;       // same layout on the device
     csv_result* d_hres = nullptr;
     uint32_t* d_hpool = nullptr;
-    // per-brick calls (n <= kBrickGraphMax): the request copy, the decode launches and the two
-    // copy-backs (into pinned staging) replayed as ONE CUDA graph, keyed by (n, voxels) and the
+    // per-brick calls (n <= kBrickGraphMax): the request copy and the decode launches (storing
+    // labels and results into mapped pinned staging) replayed as ONE CUDA graph, keyed by (n, voxels) and the
     // workspace pointers; captured on the second call with a key (the first one sizes the
     // workspace and loads the kernels), on a private stream
     struct BrickGraph {
         cudaGraphExec_t exec = nullptr;
-        uint64_t n = 0, total = 0, seen = 0;
+        uint64_t n = 0, total = 0, seen = 0, wide = 0;
         const void* ptrs[8]{};
     } bgraph[8];
     uint32_t bg_next = 0;
     cudaStream_t cap_stream = nullptr;
-    uint8_t* h_bout = nullptr;      // pinned: labels then results of a graph replay
+    uint8_t* h_bout = nullptr;      // pinned + mapped: labels then results of a graph replay (the kernels store
+                                    // into it over PCIe: no copy-back nodes)
+    std::vector<uint32_t> h_paln;   // palette length per brick (host directory only): per-brick plans skip
+                                    // the u16 replay pass when no request needs it
     uint64_t h_bout_cap = 0;
 };
 constexpr uint64_t kBrickGraphMax = 16;
@@ -366,6 +369,11 @@ static int vol_create(int device, const uint8_t* head120, const uint8_t* dir44, 
         const uint8_t* ddir = dir44;
         uint8_t* tmp = nullptr;
         if (!dir_on_device) {
+            v->h_paln.resize(n);
+            for (uint64_t i = 0; i < n; ++i) {
+                const uint8_t* r = dir44 + 44 * i + 8;
+                v->h_paln[i] = (uint32_t)r[0] | ((uint32_t)r[1] << 8) | ((uint32_t)r[2] << 16) | ((uint32_t)r[3] << 24);
+            }
             ce = dalloc(&tmp, n * 44, st);
             if (ce != cudaSuccess) { vol_release(v); return fail(CSV_E_NOMEM, "directory staging"); }
             cudaMemcpyAsync(tmp, dir44, n * 44, cudaMemcpyHostToDevice, st);
@@ -634,14 +642,32 @@ int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick,
             if (vol->h_bout) cudaFreeHost(vol->h_bout);
             vol->h_bout = nullptr;
             vol->h_bout_cap = 0;
-            CUDA_TRY(cudaMallocHost(&vol->h_bout, std::max<uint64_t>(stage, 4096)));
+            CUDA_TRY(cudaHostAlloc(&vol->h_bout, std::max<uint64_t>(stage, 4096), cudaHostAllocMapped));
             vol->h_bout_cap = std::max<uint64_t>(stage, 4096);
         }
+        void* d_bout = nullptr;   // the device's address of the mapped staging (== h_bout under UVA)
+        CUDA_TRY(cudaHostGetDevicePointer(&d_bout, vol->h_bout, 0));
+        uint32_t* const g_pool = reinterpret_cast<uint32_t*>(d_bout);
+        csv_result* const g_res = reinterpret_cast<csv_result*>(reinterpret_cast<uint8_t*>(d_bout) + res_off);
+        // u16 replay pass only if a request's palette exceeds the u8 pass's 253 labels (unknown: keep it)
+        uint64_t wide = 1;
+        if (!vol->h_paln.empty()) {
+            wide = 0;
+            for (uint64_t i = 0; i < n; ++i) {
+                const uint64_t b = (uint64_t)h_brick[i] - vol->V.brick_begin;
+                if (b >= vol->h_paln.size() || vol->h_paln[b] > 253u) wide = 1;
+            }
+        }
+        struct PalScope {   // the plan's palette bound for the launches issued below, restored after
+            csv_volume* v; uint32_t keep;
+            PalScope(csv_volume* v_, bool narrow) : v(v_), keep(v_->V.max_pal) { if (narrow && v->V.max_pal > 253u) v->V.max_pal = 253u; }
+            ~PalScope() { v->V.max_pal = keep; }
+        } pal_scope(vol, wide == 0);
         const void* ptrs[8] = {vol->h_req, vol->d_req, vol->d_hpool, vol->d_hres, vol->h_bout, vol->d_eoff,
                                vol->d_entries, vol->d_sizes};
         csv_volume::BrickGraph* g = nullptr;
         for (auto& c : vol->bgraph)
-            if (c.seen && c.n == n && c.total == total && memcmp(c.ptrs, ptrs, sizeof(ptrs)) == 0) g = &c;
+            if (c.seen && c.n == n && c.total == total && c.wide == wide && memcmp(c.ptrs, ptrs, sizeof(ptrs)) == 0) g = &c;
         if (g && g->exec) {
             CUDA_TRY(cudaGraphLaunch(g->exec, st));
             CUDA_TRY(cudaStreamSynchronize(st));
@@ -656,10 +682,8 @@ int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick,
             CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
             cudaMemcpyAsync(vol->d_req, h, req_bytes, cudaMemcpyHostToDevice, cs);
             const int rc = csv_decode_bricks(vol, n, reinterpret_cast<const uint32_t*>(vol->d_req), vol->d_req + lod_off,
-                                             reinterpret_cast<const uint64_t*>(vol->d_req + dst_off), vol->d_hpool,
-                                             vol->d_hres, reinterpret_cast<uintptr_t>(cs));
-            cudaMemcpyAsync(vol->h_bout, vol->d_hpool, out_bytes, cudaMemcpyDeviceToHost, cs);
-            cudaMemcpyAsync(vol->h_bout + res_off, vol->d_hres, n * sizeof(csv_result), cudaMemcpyDeviceToHost, cs);
+                                             reinterpret_cast<const uint64_t*>(vol->d_req + dst_off), g_pool, g_res,
+                                             reinterpret_cast<uintptr_t>(cs));
             const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
             if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
             CUDA_TRY(ce);
@@ -682,12 +706,11 @@ int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick,
         // first call with this key: run directly (sizes the workspace), remember the key
         CUDA_TRY(cudaMemcpyAsync(vol->d_req, h, req_bytes, cudaMemcpyHostToDevice, st));
         const int rc = csv_decode_bricks(vol, n, reinterpret_cast<const uint32_t*>(vol->d_req), vol->d_req + lod_off,
-                                         reinterpret_cast<const uint64_t*>(vol->d_req + dst_off), vol->d_hpool,
-                                         vol->d_hres, stream);
+                                         reinterpret_cast<const uint64_t*>(vol->d_req + dst_off), g_pool, g_res, stream);
         if (rc) return rc;
-        CUDA_TRY(cudaMemcpyAsync(h_res, vol->d_hres, n * sizeof(csv_result), cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(h_out, vol->d_hpool, out_bytes, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
+        memcpy(h_out, vol->h_bout, out_bytes);
+        memcpy(h_res, vol->h_bout + res_off, n * sizeof(csv_result));
         const void* now[8] = {vol->h_req, vol->d_req, vol->d_hpool, vol->d_hres, vol->h_bout, vol->d_eoff,
                               vol->d_entries, vol->d_sizes};
         csv_volume::BrickGraph& c = vol->bgraph[vol->bg_next++ % 8];
@@ -695,6 +718,7 @@ int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick,
         c.exec = nullptr;
         c.n = n;
         c.total = total;
+        c.wide = wide;
         c.seen = 1;
         memcpy(c.ptrs, now, sizeof(now));
         return CSV_OK;

@@ -951,8 +951,8 @@ static void launch_k1_variant(const VolView& V, const Plan& P, unsigned long lon
 }
 
 template <int MINB, bool LAT = false>
-static void launch_k1f_variant(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, uint64_t blocks,
-                               cudaStream_t st) {
+static unsigned launch_k1f_variant(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, uint64_t blocks,
+                                   cudaStream_t st) {
     static int per_sm = 0;
     if (per_sm == 0) {
         int b = 0;
@@ -964,6 +964,7 @@ static void launch_k1f_variant(const VolView& V, const Plan& P, unsigned long lo
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     k1_fast<MINB, LAT><<<(unsigned)blocks, K1_THREADS, 0, st>>>(V, P, counter);
+    return (unsigned)blocks;
 }
 
 static bool k1_old() {
@@ -972,21 +973,22 @@ static bool k1_old() {
     return v == 1;
 }
 
+// returns K1f's grid (0 for k1_streams)
 template <bool E, bool COUNT = false>
-static void launch_k1(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
+static unsigned launch_k1(const VolView& V, const Plan& P, unsigned long long* counter, int nsm, cudaStream_t st) {
     const uint64_t items = 2 * P.n;
     const uint64_t want = (items + 31) / 32;           // warps needed at one item per lane
     const uint64_t blocks = (want + K1_THREADS / 32 - 1) / (K1_THREADS / 32);
     if (E && !COUNT && V.fast_tab && !k1_old()) {
-        if (blocks > (uint64_t)nsm * K1_MINB_LATENCY) launch_k1f_variant<K1_MINB_THROUGHPUT>(V, P, counter, nsm, blocks, st);
-        else if (blocks > kK1TinyBlocks) launch_k1f_variant<K1_MINB_LATENCY>(V, P, counter, nsm, blocks, st);
-        else launch_k1f_variant<K1_MINB_LATENCY, true>(V, P, counter, nsm, blocks, st);   // per-brick calls
-        return;
+        if (blocks > (uint64_t)nsm * K1_MINB_LATENCY) return launch_k1f_variant<K1_MINB_THROUGHPUT>(V, P, counter, nsm, blocks, st);
+        if (blocks > kK1TinyBlocks) return launch_k1f_variant<K1_MINB_LATENCY>(V, P, counter, nsm, blocks, st);
+        return launch_k1f_variant<K1_MINB_LATENCY, true>(V, P, counter, nsm, blocks, st);   // per-brick calls
     }
     if (blocks > (uint64_t)nsm * K1_MINB_LATENCY)      // more than one wave of the latency variant
         launch_k1_variant<E, COUNT, K1_MINB_THROUGHPUT>(V, P, counter, nsm, blocks, st);
     else
         launch_k1_variant<E, COUNT, K1_MINB_LATENCY>(V, P, counter, nsm, blocks, st);
+    return 0;
 }
 
 }  // namespace csv
@@ -1137,11 +1139,16 @@ cudaError_t run_decode(const VolView& V, Plan P, int mode, uint64_t* sizes_tmp, 
         else k2w_launch_mode<OUT_MORTON, uint8_t, true>(Ls, V, P, counter + 1, nsm, st, -1);
         cudaEventRecord(ov->fork, st);
     }
-    if (V.entropy) launch_k1<true>(V, P, counter, nsm, st);
+    unsigned k1_grid = 0;
+    if (ovl) P.k1_started = counter + 5;
+    if (V.entropy) k1_grid = launch_k1<true>(V, P, counter, nsm, st);
     else launch_k1<false>(V, P, counter, nsm, st);
+    P.k1_started = nullptr;
     if (ovl) {   // overlap launch on the side stream, ordered after the plan, running beside K1
         Plan Po = P;
         Po.wslot0 = (uint32_t)nsm * 32u;
+        Po.k1_started = counter + 5;
+        Po.k1_grid = k1_grid;
         cudaStreamWaitEvent(ov->side, ov->fork, 0);
         if (mode == OUT_RASTER) k2w_launch_mode<OUT_RASTER, uint8_t, true>(Ls, V, Po, counter + 1, nsm, ov->side, ow);
         else k2w_launch_mode<OUT_MORTON, uint8_t, true>(Ls, V, Po, counter + 1, nsm, ov->side, ow);

@@ -83,6 +83,12 @@ struct Plan {
     uint32_t* rq;              // [n]
     unsigned long long* rq_tail;
     uint32_t wslot0;           // first wscratch warp slot of this K2w launch (the overlap launch runs beside another)
+    // overlap launch only: K1's grid and its count of started blocks.  Its warps replay bricks
+    // only once every K1 block is resident (else they could hold the SM resources a K1 block
+    // waits for while spinning on that block's bricks); otherwise they exit and the launch
+    // after K1 takes the whole queue.
+    unsigned long long* k1_started;
+    uint32_t k1_grid;
 };
 
 __device__ __forceinline__ uint64_t req_local(const VolView& V, const Plan& P, uint64_t r) {

@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_fast(VolView V, Plan P, u
     // LAT: plans of a few blocks (per-brick calls), where one lane's chain is the whole time
     __shared__ uint32_t tab[2 * 4096];
     __shared__ __align__(32) uint2 ring[K1_THREADS][4];
+    if (P.k1_started && threadIdx.x == 0) atomicAdd(P.k1_started, 1ull);   // resident (overlap launch)
     for (int i = threadIdx.x; i < 2 * 4096; i += blockDim.x) {
         const uint32_t o = V.dtab[i];   // {f:16 | (slot-cum):12 | s:4} -> {f:12 | (slot-cum):12 | 0:4 | s:4}
         tab[i] = ((o >> 16) << 20) | (((o >> 4) & 0xFFFu) << 8) | (o & 15u);

@@ -1049,6 +1049,18 @@ __global__ void __launch_bounds__(32 * K2W_WARPS, K2W_MINB) k2_warp(VolView V, P
     uint16_t* const cdesc = reinterpret_cast<uint16_t*>(base + Y.cdesc);
     uint32_t* const amask = reinterpret_cast<uint32_t*>(base + Y.amask);
     const int lane = threadIdx.x & 31;
+    if (Q && P.k1_grid) {   // overlap launch: work only beside a fully resident K1 (Plan::k1_started)
+        unsigned long long st = 0;
+        if (lane == 0) {
+            for (uint32_t spin = 0; spin < 512; ++spin) {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(st) : "l"(P.k1_started) : "memory");
+                if (st >= P.k1_grid) break;
+                __nanosleep(128);
+            }
+        }
+        st = __shfl_sync(FULL, st, 0);
+        if (st < P.k1_grid) return;
+    }
     while (true) {
         __syncwarp();
         unsigned long long rr = 0;
