@@ -136,6 +136,46 @@ def test_fuzz_resident_decode_brick(pkg, name):
             assert _gpu_outcome(pkg, c, case["brick"], int(t)) == exp[:2], (name, case, t)
 
 
+@pytest.mark.parametrize("name", ["d_b5_mem", "g_b6", "h_b3_u16"])
+def test_resident_graph_replay(pkg, oracle, name):
+    """Per-brick calls on one device-resident container: the first call of a (requests,
+    voxels) shape launches directly, the second captures the CUDA graph, later ones replay
+    it (the request copy reads the pinned staging at replay time; labels and results land
+    in mapped pinned memory).  Three passes over every brick at every LOD, bricks in a
+    shuffled order, each call vs the oracle; then a corrupted directory entry (new
+    container) raises the reference's message on the replayed path as well."""
+    data = golden_bytes(name)
+    c = pkg.CsvContainer.from_bytes(data)
+    oc = oracle.Container.from_bytes(data)
+    N = c.meta.brick_log2
+    n = c.meta.brick_count
+    rng = np.random.default_rng(11)
+    ref = {}
+    for rep in range(3):
+        for t in range(N):   # (t == N is palette[0], no decode)
+            for i in rng.permutation(n)[: min(n, 24)]:
+                i = int(i)
+                if (i, t) not in ref:
+                    ref[(i, t)] = oracle.container_decode_brick(oc, i, t)[1]
+                assert np.array_equal(c.decode_brick(i, t), ref[(i, t)]), (name, rep, i, t)
+    d = c.directory.copy()
+    d[1]["coarse_bytes"] = 2   # truncated coarse stream
+    c2 = pkg.CsvContainer.from_bytes(data)
+    c2.directory = d
+    oc2 = oracle.Container.from_bytes(data)
+    oc2.directory[1, 3] = 2   # DIR_COLS[3] == coarse_bytes
+    bad, _ = oracle.container_decode_brick(oc2, 1, 1)
+    assert bad[0] != 0
+    msgs = set()
+    for _ in range(4):   # direct, capture, replay, replay
+        with pytest.raises(pkg.CorruptStreamError) as ei:
+            c2.decode_brick(1, 1)
+        msgs.add(str(ei.value))
+        assert np.array_equal(c2.decode_brick(0, 1), oracle.container_decode_brick(oc, 0, 1)[1])
+    from paper_2308_16619_b200.device import status_error
+    assert msgs == {str(status_error(*bad[:3]))}
+
+
 def test_resident_container_follows_replacement(pkg):
     """The cached device copy is rebuilt when the directory or a blob is replaced."""
     g = golden_json("decode_d_b5_mem.json")
