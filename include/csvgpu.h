@@ -164,6 +164,22 @@ int csv_decode_bricks(csv_volume* vol, uint64_t n, const uint32_t* d_brick, cons
 int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick, const uint8_t* h_lod,
                            uint32_t* h_out, csv_result* h_res, uintptr_t stream);
 
+/* Streams passed per call: replaces decode_brick_entropy (codec.py:571-594)
+ * and decode_brick (codec.py:549-568) -> _run_decode (codec.py:498-546) for
+ * ONE brick whose palette and coarse / detail stream bytes are host arrays.
+ * head120 is the 120-byte head of a one-brick volume (dims = brick side; its
+ * count tables and entropy flag are the ones the streams were coded with;
+ * the blob sizes in it are ignored).  Decodes at LOD t into h_out
+ * (8^(N - t) labels, Morton order) and h_res (status / stream / nibble,
+ * consumed counts).  The library keeps one scratch volume per device (blobs
+ * grown on demand, re-created when the tables or brick size change) and
+ * pinned staging; thread-safe (serialised); returns after the stream has
+ * synchronised. */
+int csv_decode_brick_streams(int device, const uint8_t* head120, const uint32_t* palette, uint64_t n_pal,
+                             const uint8_t* coarse, uint64_t coarse_bytes, uint32_t coarse_nibbles,
+                             const uint8_t* detail, uint64_t detail_bytes, uint32_t detail_nibbles, int t,
+                             uint32_t* h_out, csv_result* h_res, uintptr_t stream);
+
 /* Stand-alone entropy stage (K1): replaces rans_decode/_decode_core
  * (rans.py:140-198) + iter_operations (codec.py:604-623).  For each request
  * brick, decodes the coarse and (t == 0) detail stream into entry bytes

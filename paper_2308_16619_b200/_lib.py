@@ -32,7 +32,7 @@ EXPORTS = (
     "csv_cache_mark_used", "csv_cache_assign", "csv_cache_state", "csv_cache_counters", "csv_cache_stack_heights",
     "csv_cache_read_state", "csv_cache_plan", "csv_cache_decode_fills", "csv_volume_stage_detail",
     "csv_cache_read_fills", "csv_detail_plan_greedy", "csv_rans_decode", "csv_rans_encode", "csv_build_pyramid",
-    "csv_downsample", "csv_decode_bricks_host", "csv_peer_alloc", "csv_peer_free", "csv_peer_open", "csv_peer_close",
+    "csv_downsample", "csv_decode_bricks_host", "csv_decode_brick_streams", "csv_peer_alloc", "csv_peer_free", "csv_peer_open", "csv_peer_close",
 )
 
 
@@ -146,6 +146,8 @@ def lib():
         L.csv_peer_close.argtypes = [I, P]
         L.csv_decode_bricks_host.restype = I
         L.csv_decode_bricks_host.argtypes = [P, U64, P, P, P, P, UP]
+        L.csv_decode_brick_streams.restype = I
+        L.csv_decode_brick_streams.argtypes = [I, P, P, U64, P, U64, ctypes.c_uint32, P, U64, ctypes.c_uint32, I, P, P, UP]
         L.csv_downsample.restype = I
         L.csv_downsample.argtypes = [P, I64, I64, I64, P, UP]
         _lib = L

@@ -92,8 +92,9 @@ def single_brick_head(brick_log2: int, entropy: bool, tables: TablePair | None,
 
 def _decode_one(palette, coarse, n_coarse, detail, n_detail, entropy, tables, config: BrickConfig, t,
                 return_consumed):
-    """_run_decode (codec.py:498-546) on the GPU for one brick."""
-    from .device import GpuVolume, status_error
+    """_run_decode (codec.py:498-546) on the GPU for one brick (csv_decode_brick_streams:
+    the streams through the library's pinned staging into a cached one-brick volume)."""
+    from .device import status_error
     from . import _lib
     palette = np.asarray(palette)
     if palette.size == 0:
@@ -108,27 +109,18 @@ def _decode_one(palette, coarse, n_coarse, detail, n_detail, entropy, tables, co
     pal = np.ascontiguousarray(palette, dtype=np.uint32)
     cb = np.ascontiguousarray(coarse, dtype=np.uint8)
     db = np.ascontiguousarray(detail, dtype=np.uint8)
-    row = np.zeros(1, dtype=DIRECTORY_DTYPE)
-    row["palette_len"] = pal.size
-    row["coarse_bytes"] = cb.size
-    row["coarse_nibbles"] = n_coarse
-    row["detail_bytes"] = db.size
-    row["detail_nibbles"] = n_detail
     head = single_brick_head(N, entropy, tables, pal.size, cb.size, db.size)
-    vol = GpuVolume(head, row, pal, cb, db)
-    try:
-        dev = vol.device
-        bricks = torch.zeros(1, dtype=torch.int32, device=dev)
-        lods = torch.full((1,), t, dtype=torch.uint8, device=dev)
-        dst = torch.zeros(1, dtype=torch.int64, device=dev)
-        pool = torch.empty(8 ** (N - t), dtype=torch.int32, device=dev)
-        res = vol.decode_bricks(bricks, lods, dst, pool)
-        r = GpuVolume.results_host(res, 1)[0]
-        if r["status"] != 0:
-            raise status_error(int(r["status"]), int(r["stream"]), int(r["pos"]))
-        out = pool.cpu().numpy().view(np.uint32)
-    finally:
-        vol.close()
+    dev = torch.cuda.current_device()
+    out = np.empty(8 ** (N - t), dtype=np.uint32)
+    res = np.zeros(1, dtype=_lib.RESULT_DTYPE)
+    # one C-ABI call: the library's cached one-brick scratch volume on this device
+    _lib.check(_lib.lib().csv_decode_brick_streams(dev, head, pal.ctypes.data, pal.size, cb.ctypes.data, cb.size,
+                                                    int(n_coarse), db.ctypes.data, db.size, int(n_detail), t,
+                                                    out.ctypes.data, res.ctypes.data,
+                                                    torch.cuda.current_stream(dev).cuda_stream))
+    r = res[0]
+    if r["status"] != 0:
+        raise status_error(int(r["status"]), int(r["stream"]), int(r["pos"]))
     if return_consumed:
         return out, int(r["ci"]), int(r["di"])
     return out

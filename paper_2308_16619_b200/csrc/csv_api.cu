@@ -161,6 +161,15 @@ __global__ void k_stage_detail(uint64_t* d_off, uint32_t* d_bytes, uint64_t bric
     }
 }
 
+// One-brick scratch volume (csv_decode_brick_streams): brick 0's directory row, set per call.
+__global__ void k_set_brick0(uint64_t* pal_off, uint32_t* pal_n, uint64_t* c_off, uint32_t* c_bytes, uint32_t* c_nib,
+                             uint64_t* d_off, uint32_t* d_bytes, uint32_t* d_nib, uint32_t np, uint32_t cb, uint32_t cn,
+                             uint32_t db, uint32_t dn) {
+    pal_off[0] = 0; pal_n[0] = np;
+    c_off[0] = 0; c_bytes[0] = cb; c_nib[0] = cn;
+    d_off[0] = 0; d_bytes[0] = db; d_nib[0] = dn;
+}
+
 // ---------------------------------------------------------------------------- helpers
 static int parse_head(const uint8_t* h, csv_volume* v, uint32_t* dtab_host) {
     if (memcmp(h, "CSV1", 4) != 0) return fail(CSV_E_FORMAT, "bad magic");
@@ -732,6 +741,103 @@ int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick,
     CUDA_TRY(cudaMemcpyAsync(h_out, vol->d_hpool, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     return CSV_OK;
+}
+
+// Streams passed per call (decode_brick_entropy / decode_brick): one cached one-brick
+// volume per device, re-created only when the head's tables / brick size / entropy flag
+// change or a stream outgrows its capacity; per call the streams go through pinned
+// staging into the volume's blobs, one tiny kernel sets brick 0's directory row, and
+// csv_decode_bricks_host decodes it (graph replay from the third call of a shape).
+namespace {
+struct BrickScratch {
+    uint8_t key[68]{};              // flags, brick_log2, the two count tables
+    csv_volume* vol = nullptr;
+    uint64_t cap_pal = 0, cap_c = 0, cap_d = 0;
+    uint8_t* h_stage = nullptr;     // pinned: palette | coarse | detail
+    uint64_t h_cap = 0;
+};
+BrickScratch g_scratch[64];
+std::mutex g_scratch_mu;
+}  // namespace
+
+int csv_decode_brick_streams(int device, const uint8_t* head120, const uint32_t* palette, uint64_t n_pal,
+                             const uint8_t* coarse, uint64_t coarse_bytes, uint32_t coarse_nibbles,
+                             const uint8_t* detail, uint64_t detail_bytes, uint32_t detail_nibbles, int t,
+                             uint32_t* h_out, csv_result* h_res, uintptr_t stream) {
+    if (!head120 || !h_out || !h_res || (n_pal && !palette) || (coarse_bytes && !coarse) || (detail_bytes && !detail))
+        return fail(CSV_E_ARG, "null argument");
+    if (device < 0 || device >= 64) return fail(CSV_E_ARG, "device %d out of range", device);
+    if (n_pal == 0) return fail(CSV_E_ARG, "empty palette");
+    if (n_pal > 0xffffffffull || coarse_bytes > 0xffffffffull || detail_bytes > 0xffffffffull)
+        return fail(CSV_E_ARG, "stream too long");
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    BrickScratch& S = g_scratch[device];
+    uint8_t key[68];
+    key[0] = head120[6]; key[1] = head120[10]; key[2] = head120[11]; key[3] = 0;
+    memcpy(key + 4, head120 + 32, 64);
+    auto grow = [](uint64_t need, uint64_t have) { uint64_t c = have ? have : 1024; while (c < need) c *= 2; return c; };
+    if (!S.vol || memcmp(key, S.key, sizeof key) != 0 || n_pal > S.cap_pal || coarse_bytes > S.cap_c ||
+        detail_bytes > S.cap_d) {
+        const bool same = S.vol && memcmp(key, S.key, sizeof key) == 0;
+        const uint64_t cp = grow(n_pal, same ? S.cap_pal : 0), cc = grow(coarse_bytes, same ? S.cap_c : 0),
+                       cd = grow(detail_bytes, same ? S.cap_d : 0);
+        if (S.vol) { vol_release(S.vol); S.vol = nullptr; }
+        uint8_t row[44] = {};
+        const uint32_t ucp = (uint32_t)cp, ucc = (uint32_t)cc, ucd = (uint32_t)cd;
+        memcpy(row + 8, &ucp, 4);
+        memcpy(row + 20, &ucc, 4);
+        memcpy(row + 36, &ucd, 4);
+        csv_volume* v = nullptr;
+        const int rc = vol_create(device, head120, row, false, 0, 1, nullptr, 0, cp, nullptr, 0, cc, nullptr, 0, cd, false,
+                                  stream, &v, true);
+        if (rc) return rc;
+        if (v->V.nb != 1) { vol_release(v); return fail(CSV_E_ARG, "head must describe a one-brick volume"); }
+        // entry regions: bounded by the format (<= 2 nibbles per entry of each stream)
+        v->region_max_t0 = round32(2ull * max_entries(v->V.N, 0, 0)) + round32(2ull * max_entries(v->V.N, 0, 1));
+        v->region_total_t0 = v->region_max_t0;
+        S.vol = v;
+        memcpy(S.key, key, sizeof key);
+        S.cap_pal = cp; S.cap_c = cc; S.cap_d = cd;
+    }
+    csv_volume* v = S.vol;
+    if (t < 0 || t > v->V.N) return fail(CSV_E_ARG, "LOD %d outside [0, %d]", t, v->V.N);
+    const uint64_t pb = 4 * n_pal, need = pb + coarse_bytes + detail_bytes;
+    if (need > S.h_cap) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (S.h_stage) cudaFreeHost(S.h_stage);
+        S.h_stage = nullptr;
+        S.h_cap = 0;
+        const uint64_t cap = grow(need, 0);
+        CUDA_TRY(cudaMallocHost(&S.h_stage, cap));
+        S.h_cap = cap;
+    }
+    memcpy(S.h_stage, palette, pb);
+    if (coarse_bytes) memcpy(S.h_stage + pb, coarse, coarse_bytes);
+    if (detail_bytes) memcpy(S.h_stage + pb + coarse_bytes, detail, detail_bytes);
+    CUDA_TRY(cudaMemcpyAsync(const_cast<uint32_t*>(v->V.palette), S.h_stage, pb, cudaMemcpyHostToDevice, st));
+    if (coarse_bytes)
+        CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(v->V.coarse), S.h_stage + pb, coarse_bytes, cudaMemcpyHostToDevice, st));
+    if (detail_bytes)
+        CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(v->V.detail), S.h_stage + pb + coarse_bytes, detail_bytes,
+                                 cudaMemcpyHostToDevice, st));
+    k_set_brick0<<<1, 1, 0, st>>>(const_cast<uint64_t*>(v->V.pal_off), const_cast<uint32_t*>(v->V.pal_len),
+                                  const_cast<uint64_t*>(v->V.c_off), const_cast<uint32_t*>(v->V.c_bytes),
+                                  const_cast<uint32_t*>(v->V.c_nib), const_cast<uint64_t*>(v->V.d_off),
+                                  const_cast<uint32_t*>(v->V.d_bytes), const_cast<uint32_t*>(v->V.d_nib), (uint32_t)n_pal,
+                                  (uint32_t)coarse_bytes, coarse_nibbles, (uint32_t)detail_bytes, detail_nibbles);
+    CUDA_TRY(cudaGetLastError());
+    v->V.max_pal = (uint32_t)n_pal;
+    if (!v->h_paln.empty()) v->h_paln[0] = (uint32_t)n_pal;
+    const uint32_t b0 = 0;
+    const uint8_t t8 = (uint8_t)t;
+    if (t == v->V.N) {   // coarsest LOD: palette[0], no decode (codec.py:514-516)
+        h_out[0] = palette[0];
+        memset(h_res, 0, sizeof(csv_result));
+        return CSV_OK;
+    }
+    return csv_decode_bricks_host(v, 1, &b0, &t8, h_out, h_res, stream);
 }
 
 int csv_streams_capacity(csv_volume* vol, uint64_t n, int t, uint64_t* cap) {
