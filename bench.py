@@ -343,9 +343,11 @@ def run_reference(args, world, rank):
               f"{vol.size / 1e6:.0f} MVox of the {X * Y * Z / 1e6:.0f} MVox volume); {what}")
     line = {"impl": "reference", "metric": "decoded GVoxel/s (full-volume decode, LOD 0)", "value": value,
             "unit": "GVoxel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": {"workload": wl["desc"], "brick": 32, "entropy": "rANS", "lod": 0,
-                                            "sample_voxels_per_step": int(vol.size)},
+            "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic",
+            "config": {"workload": wl["desc"], "brick": 32, "entropy": "rANS", "lod": 0,
+                       "bricks": int(np.prod([-(-d // 32) for d in wl["dims"]])),
+                       "sample_voxels_per_step": int(vol.size)},
             "step_seconds": [round(x, 4) for x in times],
             "cpu_baseline": {"value": value, "unit": "GVoxel/s", "cores": cores, "kind": kind, "sample": sample,
                              "cpu_model": cpu_model()},
