@@ -38,6 +38,9 @@
 #ifndef K1F_EVICT_FIRST
 #define K1F_EVICT_FIRST 1   // entry stores L2::evict_first (K1 DRAM reads 1.30x -> 1.18x of the stream bytes)
 #endif
+#ifndef K1F_OR_ADDR
+#define K1F_OR_ADDR 1   // table base | slot offset (16 KB-aligned tables): one instruction less per symbol
+#endif
 #ifndef K1F_BLOCK
 #define K1F_BLOCK 16
 #endif
@@ -119,11 +122,22 @@ __device__ __forceinline__ void fl_flush(FLane& L) {
     }
 }
 
-// One symbol without checks (fast blocks).
+#if K1F_OR_ADDR
+// The decode tables at file scope: their shared address is a link-time constant that folds
+// into the LDS immediate, so a slot's address is one LOP3 (s << 12 | x & 4095) + the scale.
+__shared__ uint32_t k1f_tab[2 * 4096];
+#endif
+
+// One symbol without checks (fast blocks).  L.tb: s << 12 (K1F_OR_ADDR), else the table's
+// shared byte address.
 __device__ __forceinline__ uint32_t fl_lookup(const FLane& L) {
+#if K1F_OR_ADDR
+    return k1f_tab[L.tb | (L.x & (kTotalFreq - 1u))];
+#else
     uint32_t e;
     asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(L.tb + 4u * (L.x & (kTotalFreq - 1u))));
     return e;
+#endif
 }
 
 // LAT (the single-wave variant, where the longest stream's chain sets the time): the
@@ -134,7 +148,7 @@ __device__ __forceinline__ uint32_t fl_lookup(const FLane& L) {
 template <bool LAT = false>
 __device__ __forceinline__ uint32_t fl_lookup_t(const FLane& L) {
     uint32_t e;
-    if (LAT) {
+    if (LAT && !K1F_OR_ADDR) {
         uint32_t a;
         asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a) : "r"(L.x & (kTotalFreq - 1u)), "r"(L.tb));
         asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(a));
@@ -272,7 +286,7 @@ __device__ bool fl_init(FLane& L, const VolView& V, const Plan& P, uint64_t item
     const bool ok = b < V.nb && t < V.N && !(s == 1 && t != 0);
     L.n = ok ? eff_nibbles(V, b, s) : 0;
     L.lim = ok ? stream_limit(V, b, t, s) : 0;
-    L.tb = tab_s + ((uint32_t)s << 14);
+    L.tb = K1F_OR_ADDR ? ((uint32_t)s << 12) : tab_s + ((uint32_t)s << 14);
     if (!ok) {
         P.sres[w] = csv_stream_result{0, 0xffffffffu, 0, 0};
         fl_signal(P, w);
@@ -309,7 +323,11 @@ __device__ bool fl_init(FLane& L, const VolView& V, const Plan& P, uint64_t item
 template <int MINB, bool LAT>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_fast(VolView V, Plan P, unsigned long long* counter) {
     // LAT: plans of a few blocks (per-brick calls), where one lane's chain is the whole time
+#if K1F_OR_ADDR
+    uint32_t* const tab = k1f_tab;
+#else
     __shared__ uint32_t tab[2 * 4096];
+#endif
     __shared__ __align__(32) uint2 ring[K1_THREADS][4];
     if (P.k1_started && threadIdx.x == 0) atomicAdd(P.k1_started, 1ull);   // resident (overlap launch)
     for (int i = threadIdx.x; i < 2 * 4096; i += blockDim.x) {
