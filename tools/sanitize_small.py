@@ -1,6 +1,7 @@
 """Small decode workload for compute-sanitizer runs (memcheck / racecheck / synccheck):
 config-1 container at LOD 0 and 2 (raster, K2w u8 pass), a batched Morton decode with
-mixed LODs, b=64 / b=128 containers (K2w<6>, k2_replay<7>), the per-brick resident path,
+mixed LODs, b=64 / b=128 containers (K2w<6>, k2_replay<7>), the per-brick resident path (direct, graph capture, graph replay), the streams-per-call
+scratch volume, a > 2048-request batch (K1 -> K2w overlap launch),
 the rANS / pyramid drop-ins, stats() (K1 count mode), a
 noise container whose palettes need the u16 K2w pass, and one device-cache frame with
 LOD selection, visibility and cold-detail staging."""
@@ -33,8 +34,21 @@ with open(os.path.join(G, "vol_j_b7.csv1"), "rb") as f:
     j = p.CsvContainer.from_bytes(f.read())
 p.decompress_volume(j, 0)                       # b=128 LOD 0: k2_replay<7>
 p.decompress_volume(j, 1)                       # b=128 LOD 1: K2w<6>
-for t in (0, 1, 3):                             # per-brick path on the resident container
-    c.decode_brick(5, t)
+for rep in range(3):                            # per-brick path: direct, graph capture, graph replay
+    for t in (0, 1, 3):
+        c.decode_brick(5 + rep, t)
+e0 = c.directory[5]                             # streams passed per call: the cached scratch volume
+for t in (0, 1, 3):
+    p.decode_brick_entropy(c.brick_palette(5), c.brick_coarse(5), int(e0["coarse_nibbles"]), c.brick_detail(5),
+                           int(e0["detail_nibbles"]), c.tables, t, c.config)
+# a batch of > 2048 requests: the K1 -> K2w overlap launch (ready queue, residency guard)
+nreq = 4200
+ob = (torch.arange(nreq, device="cuda") % 128).to(torch.int32)
+ol = (torch.arange(nreq, device="cuda") % 2).to(torch.uint8)
+osz = 8 ** (5 - ol.to(torch.int64))
+odst = torch.cumsum(osz, 0) - osz
+opool = torch.empty(int(osz.sum()), dtype=torch.int32, device="cuda")
+p.GpuVolume.raise_first(vol.decode_bricks(ob, ol, odst, opool), nreq)
 tab = c.tables.leaf                             # stand-alone drop-ins
 nib = np.arange(300, dtype=np.uint8) % 16
 assert np.array_equal(p.rans_decode(p.rans_encode(nib, tab), 300, tab), nib)
