@@ -330,9 +330,23 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_fast(VolView V, Plan P, u
 #endif
     __shared__ __align__(32) uint2 ring[K1_THREADS][4];
     if (P.k1_started && threadIdx.x == 0) atomicAdd(P.k1_started, 1ull);   // resident (overlap launch)
-    for (int i = threadIdx.x; i < 2 * 4096; i += blockDim.x) {
-        const uint32_t o = V.dtab[i];   // {f:16 | (slot-cum):12 | s:4} -> {f:12 | (slot-cum):12 | 0:4 | s:4}
-        tab[i] = ((o >> 16) << 20) | (((o >> 4) & 0xFFFu) << 8) | (o & 15u);
+    // {f:16 | (slot-cum):12 | s:4} -> {f:12 | (slot-cum):12 | 0:4 | s:4}
+    if (MINB >= 5) {   // throughput variant (48 registers): the plain loop
+        for (int i = threadIdx.x; i < 2 * 4096; i += blockDim.x) {
+            const uint32_t o = V.dtab[i];
+            tab[i] = ((o >> 16) << 20) | (((o >> 4) & 0xFFFu) << 8) | (o & 15u);
+        }
+    } else {   // single-wave / per-brick variants: all 8 vector loads of a thread in flight at once
+        static_assert(2 * 4096 == 8 * 4 * K1_THREADS, "table fill: 8 uint4 per thread");
+        const uint4* const src = reinterpret_cast<const uint4*>(V.dtab);
+        uint4 w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = __ldg(src + k * K1_THREADS + threadIdx.x);
+        auto cv = [](uint32_t o) { return ((o >> 16) << 20) | (((o >> 4) & 0xFFFu) << 8) | (o & 15u); };
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            reinterpret_cast<uint4*>(tab)[k * K1_THREADS + threadIdx.x] =
+                make_uint4(cv(w[k].x), cv(w[k].y), cv(w[k].z), cv(w[k].w));
     }
     __syncthreads();
     const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab);
