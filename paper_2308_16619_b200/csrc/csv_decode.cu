@@ -1064,9 +1064,10 @@ static void k2w_launch_mode(int L, const VolView& V, const Plan& P, unsigned lon
     }
 }
 // K1 -> K2w overlap: CSVGPU_OVERLAP=0 disables it; CSVGPU_OVL_WARPS overrides the overlap
-// launch's warps per SM.  Default: 16 when K1 has at most 2 blocks per SM (strong-scaling
-// shares of <= 8 bz layers), else 12 (measured on the config-3 shares and the config-4 batch;
-// more warps than fit beside K1 take the SMs K1's finished blocks leave).
+// launch's warps per SM.  Default 32 (the whole upper half of the wscratch slots): the CTAs
+// that do not fit beside K1 queue and take the SMs K1's finished blocks leave, so the
+// overlap launch becomes the full-occupancy replay as K1 drains (config-4 batch and the
+// config-3 shares measured at 4 / 8 / 12 / 16 / 24 / 32 warps).
 static int ovl_warps(uint64_t k1_blocks, int nsm) {
     static int v = -2;
     if (v == -2) {
@@ -1077,7 +1078,8 @@ static int ovl_warps(uint64_t k1_blocks, int nsm) {
         if (v > 32) v = 32;
     }
     if (v >= 0) return v;
-    return k1_blocks <= 2ull * (uint64_t)nsm ? 16 : 12;
+    (void)k1_blocks; (void)nsm;
+    return 32;
 }
 static bool k2w6_disabled() {
     static int v = -1;
