@@ -679,6 +679,39 @@ def run_ours(args, world, rank, local):
     }
     if gather is not None:
         line["decode_gather"] = gather
+    # ---- e2e: public API, host buffers in, host volume out (pinned)
+    if not args.no_e2e and not args.profile:
+        try:                                   # one pinned 34 GB volume per rank; pageable if the host refuses
+            pin = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32, pin_memory=True)
+        except RuntimeError:
+            pin = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32)
+        times = []
+        pin_np = pin.numpy().view(np.uint32)
+        layers = None if weak else plan["layers"]
+        # one untimed call first: the freshly pinned pages' first device writes (IOMMU / page
+        # setup) cost the first one or two calls up to 2x
+        p.decompress_volume(cont, 0, out=pin_np, layers=layers)
+        for it in range(5):
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
+            # the reference-facing API, host container in / host (slab of the) volume out
+            p.decompress_volume(cont, 0, out=pin_np, layers=layers)
+            times.append(time.perf_counter() - t0)
+        e2e_s = max_over_ranks(min(times), world)
+        h2d = sum_over_ranks(44 * n_b + pal_b + cb_b + db_b, world)
+        d2h = sum_over_ranks(4 * voxels_rank, world)
+        line["e2e"] = {"value": voxels_all / e2e_s / 1e9, "unit": "GVoxel/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "seconds": e2e_s,
+                       "seconds_all": [round(x, 4) for x in times],
+                       "reduction": "best of 5 after one untimed call (host-timed, synchronised), max over ranks",
+                       "path": "decompress_volume(container, 0, out=pinned host array%s): H2D of directory+blobs, "
+                               "slab-pipelined GPU decode overlapped with D2H into the pinned (Z,Y,X) uint32 %s" %
+                               (", layers=this rank's bz range" if layers else "",
+                                "slab of each rank" if layers and world > 1 else "volume")}
+        e2e_check = check_bricks(blocks, pin, zr[0], brick_range[0], brick_range[1], grid)
+        line["e2e"]["check"] = e2e_check
+        del pin
     # ---- config 4: batched random-access decode into a device brick pool
     cache_reqs = None
     if not args.no_cache and not args.profile and (world == 1 or not weak):
@@ -804,36 +837,6 @@ def run_ours(args, world, rank, local):
     # ---- config 5: the 16-timestep ensemble encode + decode, timesteps sharded over the ranks
     if not args.no_cache and not args.profile and args.workload == "config3" and not args.zlayers:
         line["timeseries"] = timeseries_leg(p, torch, dev, stream, world, rank)
-    # ---- e2e: public API, host buffers in, host volume out (pinned)
-    if not args.no_e2e and not args.profile:
-        try:                                   # one pinned 34 GB volume per rank; pageable if the host refuses
-            pin = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32, pin_memory=True)
-        except RuntimeError:
-            pin = torch.empty((zr[1] - zr[0], Y, X), dtype=torch.int32)
-        times = []
-        pin_np = pin.numpy().view(np.uint32)
-        layers = None if weak else plan["layers"]
-        for it in range(5):
-            torch.cuda.synchronize()
-            barrier(world)
-            t0 = time.perf_counter()
-            # the reference-facing API, host container in / host (slab of the) volume out
-            p.decompress_volume(cont, 0, out=pin_np, layers=layers)
-            times.append(time.perf_counter() - t0)
-        e2e_s = max_over_ranks(min(times), world)
-        h2d = sum_over_ranks(44 * n_b + pal_b + cb_b + db_b, world)
-        d2h = sum_over_ranks(4 * voxels_rank, world)
-        line["e2e"] = {"value": voxels_all / e2e_s / 1e9, "unit": "GVoxel/s", "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": d2h, "seconds": e2e_s,
-                       "seconds_all": [round(x, 4) for x in times],
-                       "reduction": "best of 5 (host-timed, synchronised), max over ranks",
-                       "path": "decompress_volume(container, 0, out=pinned host array%s): H2D of directory+blobs, "
-                               "slab-pipelined GPU decode overlapped with D2H into the pinned (Z,Y,X) uint32 %s" %
-                               (", layers=this rank's bz range" if layers else "",
-                                "slab of each rank" if layers and world > 1 else "volume")}
-        e2e_check = check_bricks(blocks, pin, zr[0], brick_range[0], brick_range[1], grid)
-        line["e2e"]["check"] = e2e_check
-        del pin
     if not args.no_cpu and not args.profile and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baselines(wl, cache_reqs)
     if rank == 0:
