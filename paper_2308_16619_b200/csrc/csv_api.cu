@@ -92,6 +92,7 @@ struct csv_volume {
     } bgraph[8];
     uint32_t bg_next = 0;
     cudaStream_t cap_stream = nullptr;
+    std::mutex host_mu;             // csv_decode_bricks_host: staging buffers and graphs are per volume
     uint8_t* h_bout = nullptr;      // pinned + mapped: labels then results of a graph replay (the kernels store
                                     // into it over PCIe: no copy-back nodes)
     std::vector<uint32_t> h_paln;   // palette length per brick (host directory only): per-brick plans skip
@@ -608,6 +609,7 @@ int csv_decode_bricks_host(csv_volume* vol, uint64_t n, const uint32_t* h_brick,
                            uint32_t* h_out, csv_result* h_res, uintptr_t stream) {
     if (!vol || (n && (!h_brick || !h_lod || !h_out || !h_res))) return fail(CSV_E_ARG, "null argument");
     if (n == 0) return CSV_OK;
+    std::lock_guard<std::mutex> lk(vol->host_mu);   // ctypes drops the GIL: calls from two threads share the staging
     CUDA_TRY(cudaSetDevice(vol->device));
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const uint64_t lod_off = (4 * n + 15) & ~15ull, dst_off = (lod_off + n + 15) & ~15ull, req_bytes = dst_off + 8 * n;

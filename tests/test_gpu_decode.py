@@ -176,6 +176,32 @@ def test_resident_graph_replay(pkg, oracle, name):
     assert msgs == {str(status_error(*bad[:3]))}
 
 
+def test_resident_decode_brick_threads(pkg, oracle):
+    """decode_brick from four Python threads on one container (ctypes drops the GIL; the
+    per-volume staging and graphs are serialised in csv_decode_bricks_host)."""
+    import threading
+    data = golden_bytes("d_b5_mem")
+    c = pkg.CsvContainer.from_bytes(data)
+    oc = oracle.Container.from_bytes(data)
+    n = c.meta.brick_count
+    ref = {(i, t): oracle.container_decode_brick(oc, i, t)[1] for i in range(n) for t in (0, 1, 2)}
+    bad = []
+
+    def work(seed):
+        rng = np.random.default_rng(seed)
+        for _ in range(60):
+            i, t = int(rng.integers(n)), int(rng.integers(3))
+            if not np.array_equal(c.decode_brick(i, t), ref[(i, t)]):
+                bad.append((seed, i, t))
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for th in ts:
+        th.start()
+    for th in ts:
+        th.join()
+    assert not bad, bad[:5]
+
+
 def test_resident_container_follows_replacement(pkg):
     """The cached device copy is rebuilt when the directory or a blob is replaced."""
     g = golden_json("decode_d_b5_mem.json")
