@@ -375,6 +375,10 @@ __device__ __forceinline__ bool lane_step(Lane& L, const Plan& P, const uint32_t
 // longest lane's chain (latency): 9.5 vs 10.6 ms on config 3, 1.12 vs 1.17 ms on config 2.
 constexpr int K1_MINB_THROUGHPUT = 5;
 constexpr int K1_MINB_LATENCY = 3;
+// K1f (the rANS lanes of csv_k1fast.cuh) reverses that: at 48 registers its step schedules
+// worse than at the ~62 it takes when allowed 64, so multi-wave plans run 4 blocks/SM of the
+// 64-register build (config 3: K1 6.05 -> 5.72 ms; config-4 batch K1 3.3 -> 2.4 ms)
+constexpr int K1F_MINB_MULTI = 4;
 constexpr uint64_t kK1TinyBlocks = 8;   // plans of <= 8 K1 blocks (<= 1024 requests) use the latency-optimised steps
 template <bool ENTROPY, bool COUNT, int MINB>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_streams(VolView V, Plan P, unsigned long long* counter) {
@@ -980,7 +984,7 @@ static unsigned launch_k1(const VolView& V, const Plan& P, unsigned long long* c
     const uint64_t want = (items + 31) / 32;           // warps needed at one item per lane
     const uint64_t blocks = (want + K1_THREADS / 32 - 1) / (K1_THREADS / 32);
     if (E && !COUNT && V.fast_tab && !k1_old()) {
-        if (blocks > (uint64_t)nsm * K1_MINB_LATENCY) return launch_k1f_variant<K1_MINB_THROUGHPUT>(V, P, counter, nsm, blocks, st);
+        if (blocks > (uint64_t)nsm * K1_MINB_LATENCY) return launch_k1f_variant<K1F_MINB_MULTI>(V, P, counter, nsm, blocks, st);
         if (blocks > kK1TinyBlocks) return launch_k1f_variant<K1_MINB_LATENCY>(V, P, counter, nsm, blocks, st);
         return launch_k1f_variant<K1_MINB_LATENCY, true>(V, P, counter, nsm, blocks, st);   // per-brick calls
     }
