@@ -724,6 +724,8 @@ def run_ours(args, world, rank, local):
         e2e_check = check_bricks(blocks, pin, zr[0], brick_range[0], brick_range[1], grid)
         line["e2e"]["check"] = e2e_check
         del pin, pins_in, cont_h
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()   # the slab buffers (2 x 4.3 GB) back to the device before the cache legs
     # ---- config 4: batched random-access decode into a device brick pool
     cache_reqs = None
     if not args.no_cache and not args.profile and (world == 1 or not weak):
